@@ -1,0 +1,173 @@
+"""ctypes binding of libspasm.so (the C-ABI in include/spasm.h).
+
+There is deliberately no CPU fallback: if the shared library is missing, or a call is
+made without a CUDA device, this module raises. The library is built in-tree by
+``__graft_entry__.build()`` (``make -C paper_2510_07674_b200/csrc``).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from ctypes import POINTER, c_char_p, c_double, c_int, c_int32, c_int64, c_uint8, c_uint32, c_uint64, c_void_p
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libspasm.so")
+
+SPASM_OK = 0
+SPASM_NO_SOLUTION = 1
+SPASM_LIFT_FAILURE = 2
+SPASM_AL_FAILURE = 3
+SPASM_ERR_USAGE = 100
+SPASM_ERR_CUDA = 101
+
+F32 = 0
+F64 = 1
+LINEAR_ID = 0
+QUADRATIC_ID = 1
+SAMPLER_PCG64 = 0
+SAMPLER_PHILOX = 1
+
+
+class NativeError(RuntimeError):
+    """A CUDA or internal failure reported by libspasm."""
+
+
+class spasm_solve_config(ctypes.Structure):
+    _fields_ = [
+        ("n", c_int64),
+        ("m", c_int64),
+        ("k_lin", c_int32),
+        ("k_quad", c_int32),
+        ("eta_init", c_double),
+        ("alpha", c_double),
+        ("epsilon", c_double),
+        ("p_return", c_int32),
+        ("max_restarts", c_int32),
+        ("seed", c_uint64),
+        ("sampler", c_int32),
+        ("n_traced", c_int32),
+    ]
+
+
+class spasm_solve_report(ctypes.Structure):
+    _fields_ = [
+        ("success", c_int32),
+        ("restarts", c_int32),
+        ("steps", c_int32),
+        ("n_satisfying", c_int32),
+        ("flagged", c_int32),
+        ("n_chosen", c_int32),
+        ("launches", c_int32),
+        ("reserved", c_int32),
+        ("device_ms", c_double),
+    ]
+
+
+# name -> (restype, argtypes); the full exported surface of include/spasm.h
+SIGNATURES = {
+    "spasm_last_error": (c_char_p, []),
+    "spasm_version": (c_int, []),
+    "spasm_tetris_model_create": (
+        c_int,
+        [POINTER(c_void_p), c_int, c_void_p, c_void_p, c_void_p, c_int, c_void_p, c_void_p, c_void_p,
+         c_double, c_double, c_double, c_double, c_int, c_void_p, c_void_p],
+    ),
+    "spasm_tower_model_create": (
+        c_int,
+        [POINTER(c_void_p), c_int, c_double, c_double, c_void_p, c_int, c_void_p, c_void_p, c_double, c_double,
+         c_double, c_int, c_void_p, c_void_p],
+    ),
+    "spasm_model_destroy": (None, [c_void_p]),
+    "spasm_model_dimension": (c_int, [c_void_p]),
+    "spasm_evaluate": (c_int, [c_void_p, c_int, c_void_p, c_int64, c_int, c_void_p, c_void_p]),
+    "spasm_gradient": (c_int, [c_void_p, c_int, c_void_p, c_int64, c_int, c_void_p, c_void_p]),
+    "spasm_pcg64_state": (c_int, [c_uint64, c_uint64, POINTER(c_uint64)]),
+    "spasm_sample": (
+        c_int,
+        [c_int, c_int, c_void_p, c_void_p, c_uint64, c_uint64, c_int, c_int64, c_int64, c_void_p, c_int64,
+         c_void_p, c_void_p],
+    ),
+    "spasm_sample_eval": (
+        c_int,
+        [c_void_p, c_int, c_uint64, c_uint64, c_int, c_int64, c_int64, c_void_p, c_int64, c_void_p, c_void_p,
+         c_void_p, c_void_p],
+    ),
+    "spasm_step": (
+        c_int,
+        [c_int, c_void_p, c_void_p, c_int64, c_int, c_double, c_void_p, c_void_p, c_void_p, c_void_p],
+    ),
+    "spasm_descent_schedule": (
+        c_int,
+        [c_void_p, c_int, c_void_p, c_void_p, c_int64, c_int, c_int, c_double, c_double, c_double, c_void_p,
+         c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_int, c_void_p],
+    ),
+    "spasm_sort_workspace_bytes": (c_int64, [c_int, c_int64]),
+    "spasm_sort_pairs": (c_int, [c_int, c_void_p, c_void_p, c_int64, c_void_p, c_void_p]),
+    "spasm_cost_keys": (c_int, [c_int, c_void_p, c_int64, c_double, c_void_p, c_void_p, c_void_p, c_void_p]),
+    "spasm_solve_workspace_bytes": (c_int64, [c_void_p, c_int, POINTER(spasm_solve_config), c_int64]),
+    "spasm_solve": (
+        c_int,
+        [c_void_p, c_int, POINTER(spasm_solve_config), c_void_p, c_int64, c_void_p, c_int64, c_void_p, c_void_p,
+         c_void_p, POINTER(spasm_solve_report), c_void_p, c_void_p, c_void_p, c_void_p],
+    ),
+}
+
+_lib = None
+
+
+def load() -> ctypes.CDLL:
+    """Load libspasm.so once; raise loudly if it was not built."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(
+            f"{LIB_PATH} is missing: build it with __graft_entry__.build() "
+            "(make -C paper_2510_07674_b200/csrc). There is no CPU fallback."
+        )
+    lib = ctypes.CDLL(LIB_PATH)
+    for name, (res, args) in SIGNATURES.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    _lib = lib
+    return lib
+
+
+def last_error() -> str:
+    msg = load().spasm_last_error()
+    return msg.decode() if msg else ""
+
+
+def check(status: int, what: str = "") -> int:
+    """Map a C status to the reference's exception conventions."""
+    if status in (SPASM_OK, SPASM_NO_SOLUTION, SPASM_LIFT_FAILURE, SPASM_AL_FAILURE):
+        return status
+    msg = last_error()
+    if status == SPASM_ERR_USAGE:
+        raise ValueError(f"{what}: {msg}" if what else msg)
+    raise NativeError(f"{what}: {msg} (status {status})" if what else f"{msg} (status {status})")
+
+
+def ptr(t) -> int:
+    """Raw data pointer of a torch tensor or numpy array (None -> NULL)."""
+    if t is None:
+        return None
+    if isinstance(t, np.ndarray):
+        return t.ctypes.data
+    return t.data_ptr()
+
+
+def stream_handle(device=None) -> int:
+    import torch
+
+    return torch.cuda.current_stream(device).cuda_stream
+
+
+def require_cuda():
+    import torch
+
+    if not torch.cuda.is_available():
+        raise NativeError("no CUDA device: the SPaSM B200 kernels have no CPU fallback")

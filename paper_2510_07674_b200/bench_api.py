@@ -1,0 +1,81 @@
+"""Pipeline composition: the reference's ``bench.solve_scene`` boundary
+(reference bench.py:74-268) on top of the GPU engine.
+
+``solve_scene`` times stage 1 (plus lifting and the AL trajectory solve when the scene
+carries a robot) exactly where the reference does: from the start of stage 1 to the
+result, excluding scene load and the final independent validation.
+"""
+from __future__ import annotations
+
+import math
+import time
+from dataclasses import dataclass, replace
+from typing import Optional
+
+import numpy as np
+
+from .particle_opt import OptimizerConfig, solve
+from .problems import MotionProblem, Scene, as_cost_model
+
+STEP_CAP = 30000
+_TRAJ_STREAM = 1 << 20
+
+
+def effective_max_restarts(config: OptimizerConfig) -> int:
+    """Largest restart count whose total step budget fits STEP_CAP (bench.py:80-85)."""
+    per = config.k_lin + config.k_quad
+    if per == 0:
+        return config.max_restarts
+    return min(config.max_restarts, max(1, STEP_CAP // per))
+
+
+def _solver_config(scene: Scene, seed, solver_overrides, quadratic_only) -> OptimizerConfig:
+    merged = dict(scene.solver_overrides)
+    if solver_overrides:
+        merged.update(solver_overrides)
+    if quadratic_only:
+        merged["k_lin"] = 0
+    return OptimizerConfig(seed=seed, **merged)
+
+
+@dataclass
+class SceneSolution:
+    success: bool
+    time_ms: float
+    restarts: int
+    steps: int
+    final_cost: float
+    placement: Optional[np.ndarray] = None
+    trajectory: object = None
+    path_length: Optional[float] = None
+    max_violation: Optional[float] = None
+
+
+def solve_scene(scene: Scene, *, seed: int = 0, threads: int = 1, solver_overrides: Optional[dict] = None,
+                trajopt_overrides: Optional[dict] = None, quadratic_only: bool = False, no_trajopt: bool = False,
+                warm_seeds=None, precision: str = "fp32", model=None) -> SceneSolution:
+    """Run the pipeline once; failures are normal returns (bench.py:168-268)."""
+    if isinstance(scene.problem, MotionProblem):
+        if no_trajopt:
+            raise ValueError("point-to-point scenes have no placement stage")
+        from .trajopt import solve_motion_scene
+
+        return solve_motion_scene(scene, seed, trajopt_overrides, precision=precision)
+    model = model if model is not None else as_cost_model(scene.problem, precision=precision)
+    config = _solver_config(scene, seed, solver_overrides, quadratic_only)
+    config = replace(config, max_restarts=effective_max_restarts(config))
+    run_stage2 = scene.chain is not None and not no_trajopt
+    t0 = time.perf_counter()
+    result = solve(model, config, warm_seeds=warm_seeds, threads=threads)
+    if not result.success:
+        return SceneSolution(False, (time.perf_counter() - t0) * 1e3, result.report.restarts, result.report.steps,
+                             math.nan)
+    if not run_stage2:
+        time_ms = (time.perf_counter() - t0) * 1e3
+        best = result.particles[0]
+        ok = bool(np.asarray(model.satisfaction(best[None, :], config.epsilon))[0])
+        return SceneSolution(ok, time_ms, result.report.restarts, result.report.steps, float(result.costs[0]),
+                             placement=best.copy())
+    from .trajopt import solve_stage2
+
+    return solve_stage2(scene, result, config, seed, trajopt_overrides, t0, precision=precision)

@@ -1,0 +1,607 @@
+// extern "C" boundary of libspasm.so (declared in include/spasm.h).
+//
+// Also hosts the native stage-1 restart loop (spasm_solve), the C++ equivalent of
+// particle_opt.solve (reference particle_opt.py:303-400): per restart it launches
+// sample+evaluate, the stable top-M sort, the fused descent schedule, the satisfying
+// ordering and the re-check, then reads back one small result block.
+#include <algorithm>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/spasm.h"
+#include "model.hpp"
+#include "rng.cuh"
+#include "scene.cuh"
+
+namespace spasm {
+
+static thread_local std::string g_last_error;
+void set_last_error(const std::string& msg) { g_last_error = msg; }
+const char* last_error() { return g_last_error.c_str(); }
+
+void seedseq_pcg64(uint64_t seed, const uint64_t* spawn_key, int n_spawn, uint64_t out[4]);
+
+// ---- launchers (explicitly instantiated in stage1_f32.cu / stage1_f64.cu) ----------
+template <typename R> int launch_evaluate(const Model&, const R*, int64_t, int, R*, cudaStream_t);
+template <typename R> int launch_gradient(const Model&, const R*, int64_t, int, R*, cudaStream_t);
+template <typename R>
+int launch_sample_eval(const Model&, const Pcg64State&, int64_t, int64_t, const double*, int64_t, int, uint64_t,
+                       uint32_t, R*, typename KeyOf<R>::type*, uint32_t*, cudaStream_t);
+template <typename R>
+int launch_schedule(const Model&, const R*, const uint32_t*, int64_t, int, int, double, double, double, R*, R*,
+                    uint8_t*, unsigned int*, R*, uint8_t*, int, cudaStream_t);
+template <typename R>
+int launch_sample(const Bounds64&, int, const Pcg64State&, int64_t, int64_t, const double*, int64_t, int, uint64_t,
+                  uint32_t, R*, cudaStream_t);
+template <typename R>
+int launch_step(R*, const R*, int64_t, int, R, const R*, const R*, uint8_t*, cudaStream_t);
+template <typename R>
+int launch_sort(typename KeyOf<R>::type*, uint32_t*, typename KeyOf<R>::type*, uint32_t*, int64_t, unsigned int*,
+                bool*, cudaStream_t);
+template <typename R>
+int launch_sat_keys(const R*, int64_t, double, typename KeyOf<R>::type*, uint32_t*, unsigned int*, cudaStream_t);
+
+extern template int launch_evaluate<float>(const Model&, const float*, int64_t, int, float*, cudaStream_t);
+extern template int launch_evaluate<double>(const Model&, const double*, int64_t, int, double*, cudaStream_t);
+
+static Pcg64State restart_state(uint64_t seed, uint64_t restart) {
+  uint64_t o[4];
+  seedseq_pcg64(seed, &restart, 1, o);
+  Pcg64State s;
+  s.state_hi = o[0];
+  s.state_lo = o[1];
+  s.inc_hi = o[2];
+  s.inc_lo = o[3];
+  return s;
+}
+
+static inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+// ---- small helper kernels for the solve loop --------------------------------------
+template <typename R>
+__global__ void k_gather_chosen(const uint32_t* __restrict__ order, const unsigned int* __restrict__ n_sat, int p_return,
+                                const R* __restrict__ opt_values, const R* __restrict__ opt_cost,
+                                const uint32_t* __restrict__ top_idx, int D, R* __restrict__ chosen_vals,
+                                double* __restrict__ out_vals, double* __restrict__ out_cost,
+                                int32_t* __restrict__ out_idx) {
+  const int c = blockIdx.x;
+  const int k = min((int)*n_sat, p_return);
+  if (c >= p_return) return;
+  const uint32_t pos = c < k ? order[c] : 0u;
+  for (int d = threadIdx.x; d < D; d += blockDim.x) {
+    const R v = opt_values[(int64_t)pos * D + d];
+    chosen_vals[(int64_t)c * D + d] = v;
+    out_vals[(int64_t)c * D + d] = (double)v;
+  }
+  if (threadIdx.x == 0) {
+    out_cost[c] = (double)opt_cost[pos];
+    out_idx[c] = c < k ? (int32_t)top_idx[pos] : -1;
+  }
+}
+
+template <typename R>
+__global__ void k_copy_recheck(const R* __restrict__ c, int n, double* __restrict__ out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = (double)c[i];
+}
+
+__global__ void k_trace_ids(const uint32_t* __restrict__ top, int n, int32_t* __restrict__ ids) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) ids[i] = (int32_t)top[i];
+}
+
+// ---- workspace layout -------------------------------------------------------------
+struct SolveLayout {
+  size_t values, keys0, keys1, idx0, idx1, hist, opt_values, opt_cost, flagged, counters, skeys0, skeys1, svals0,
+      svals1, chosen_vals, recheck, warm, res, total;
+  size_t res_bytes;
+  int64_t n, m;
+  int D, p;
+};
+
+static size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
+
+template <typename R>
+static SolveLayout make_layout(int D, const spasm_solve_config& cfg, int64_t n_warm) {
+  using K = typename KeyOf<R>::type;
+  SolveLayout L;
+  L.n = cfg.n;
+  L.m = cfg.m;
+  L.D = D;
+  L.p = cfg.p_return;
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    size_t o = off;
+    off = align_up(off + bytes);
+    return o;
+  };
+  const int64_t tiles = (std::max(cfg.n, cfg.m) + 2047) / 2048 + 1;
+  L.values = take((size_t)cfg.n * D * sizeof(R));
+  L.keys0 = take((size_t)cfg.n * sizeof(K));
+  L.keys1 = take((size_t)cfg.n * sizeof(K));
+  L.idx0 = take((size_t)cfg.n * 4);
+  L.idx1 = take((size_t)cfg.n * 4);
+  L.hist = take((size_t)tiles * 256 * 4);
+  L.opt_values = take((size_t)cfg.m * D * sizeof(R));
+  L.opt_cost = take((size_t)cfg.m * sizeof(R));
+  L.flagged = take((size_t)cfg.m);
+  L.counters = take(64);
+  L.skeys0 = take((size_t)cfg.m * sizeof(K));
+  L.skeys1 = take((size_t)cfg.m * sizeof(K));
+  L.svals0 = take((size_t)cfg.m * 4);
+  L.svals1 = take((size_t)cfg.m * 4);
+  L.chosen_vals = take((size_t)cfg.p_return * D * sizeof(R));
+  L.recheck = take((size_t)cfg.p_return * sizeof(R));
+  L.warm = take((size_t)std::max<int64_t>(n_warm, 1) * D * 8);
+  // result block: counters(64B) | out_vals p*D doubles | out_cost p doubles | recheck p doubles | idx p int32
+  L.res_bytes = 64 + (size_t)cfg.p_return * D * 8 + (size_t)cfg.p_return * 8 * 2 + (size_t)cfg.p_return * 4;
+  L.res = take(L.res_bytes);
+  L.total = off;
+  return L;
+}
+
+static int validate_cfg(const spasm_solve_config* cfg) {
+  SPASM_REQUIRE(cfg != nullptr, "null solve config");
+  SPASM_REQUIRE(cfg->m >= 1 && cfg->m <= cfg->n, "need 1 <= m <= n");
+  SPASM_REQUIRE(cfg->n <= (int64_t)0xFFFFFFFF, "n exceeds 2^32 rows");
+  SPASM_REQUIRE(cfg->k_lin >= 0 && cfg->k_quad >= 0, "step counts must be nonnegative");
+  SPASM_REQUIRE(cfg->eta_init > 0 && cfg->alpha > 0, "learning rates must be positive");
+  SPASM_REQUIRE(cfg->epsilon > 0, "epsilon must be positive");
+  SPASM_REQUIRE(cfg->p_return >= 1, "p_return must be >= 1");
+  SPASM_REQUIRE(cfg->max_restarts >= 1, "max_restarts must be >= 1");
+  SPASM_REQUIRE(cfg->n_traced >= 0 && cfg->n_traced <= cfg->m, "n_traced must be in [0, m]");
+  return SPASM_OK;
+}
+
+template <typename R>
+static int solve_impl(Model& m, const spasm_solve_config& cfg, const double* warm_host, int64_t n_warm, void* ws,
+                      int64_t ws_bytes, double* particles, double* costs, int64_t* indices, spasm_solve_report* rep,
+                      R* trace_cost, uint8_t* trace_sat, int32_t* trace_ids, cudaStream_t s) {
+  using K = typename KeyOf<R>::type;
+  const int D = m.dim;
+  SolveLayout L = make_layout<R>(D, cfg, n_warm);
+  SPASM_REQUIRE(ws != nullptr && (size_t)ws_bytes >= L.total, "solve workspace too small");
+  SPASM_REQUIRE(n_warm >= 0 && n_warm <= cfg.n, "more warm seeds than particles");
+  char* base = static_cast<char*>(ws);
+  R* values = reinterpret_cast<R*>(base + L.values);
+  K* keys0 = reinterpret_cast<K*>(base + L.keys0);
+  K* keys1 = reinterpret_cast<K*>(base + L.keys1);
+  uint32_t* idx0 = reinterpret_cast<uint32_t*>(base + L.idx0);
+  uint32_t* idx1 = reinterpret_cast<uint32_t*>(base + L.idx1);
+  unsigned int* hist = reinterpret_cast<unsigned int*>(base + L.hist);
+  R* opt_values = reinterpret_cast<R*>(base + L.opt_values);
+  R* opt_cost = reinterpret_cast<R*>(base + L.opt_cost);
+  uint8_t* flagged = reinterpret_cast<uint8_t*>(base + L.flagged);
+  K* sk0 = reinterpret_cast<K*>(base + L.skeys0);
+  K* sk1 = reinterpret_cast<K*>(base + L.skeys1);
+  uint32_t* sv0 = reinterpret_cast<uint32_t*>(base + L.svals0);
+  uint32_t* sv1 = reinterpret_cast<uint32_t*>(base + L.svals1);
+  R* chosen_vals = reinterpret_cast<R*>(base + L.chosen_vals);
+  R* recheck = reinterpret_cast<R*>(base + L.recheck);
+  double* warm_dev = reinterpret_cast<double*>(base + L.warm);
+  char* res = base + L.res;
+  unsigned int* counters = reinterpret_cast<unsigned int*>(res);  // [0]=n_sat [1]=flagged
+  double* out_vals = reinterpret_cast<double*>(res + 64);
+  double* out_cost = out_vals + (size_t)cfg.p_return * D;
+  double* out_recheck = out_cost + cfg.p_return;
+  int32_t* out_idx = reinterpret_cast<int32_t*>(out_recheck + cfg.p_return);
+
+  if (m.pinned_bytes < L.res_bytes) {
+    if (m.pinned) cudaFreeHost(m.pinned);
+    m.pinned = nullptr;
+    m.pinned_bytes = 0;
+    SPASM_CUDA_TRY(cudaMallocHost(&m.pinned, L.res_bytes));
+    m.pinned_bytes = L.res_bytes;
+  }
+  char* host = static_cast<char*>(m.pinned);
+
+  if (n_warm > 0)
+    SPASM_CUDA_TRY(cudaMemcpyAsync(warm_dev, warm_host, (size_t)n_warm * D * 8, cudaMemcpyHostToDevice, s));
+
+  cudaEvent_t e0, e1;
+  SPASM_CUDA_TRY(cudaEventCreate(&e0));
+  SPASM_CUDA_TRY(cudaEventCreate(&e1));
+  SPASM_CUDA_TRY(cudaEventRecord(e0, s));
+
+  int total_steps = 0, total_flagged = 0, launches = 0;
+  const int per_restart = cfg.k_lin + cfg.k_quad;
+  int rc = SPASM_NO_SOLUTION;
+  std::memset(rep, 0, sizeof(*rep));
+  for (int restart = 0; restart < cfg.max_restarts; ++restart) {
+    const Pcg64State st = restart_state(cfg.seed, (uint64_t)restart);
+    int r = launch_sample_eval<R>(m, st, 0, cfg.n, n_warm ? warm_dev : nullptr, n_warm, cfg.sampler, cfg.seed,
+                                  (uint32_t)restart, values, keys0, idx0, s);
+    if (r) return r;
+    bool in1 = false;
+    if ((r = launch_sort<R>(keys0, idx0, keys1, idx1, cfg.n, hist, &in1, s))) return r;
+    const uint32_t* top = in1 ? idx1 : idx0;
+    SPASM_CUDA_TRY(cudaMemsetAsync(res, 0, 64, s));
+    const bool tr = trace_cost != nullptr && cfg.n_traced > 0;
+    if ((r = launch_schedule<R>(m, values, top, cfg.m, cfg.k_lin, cfg.k_quad, cfg.eta_init, cfg.alpha, cfg.epsilon,
+                                opt_values, opt_cost, flagged, counters + 1, tr ? trace_cost : nullptr,
+                                tr ? trace_sat : nullptr, tr ? cfg.n_traced : 0, s)))
+      return r;
+    if (tr && trace_ids) {
+      k_trace_ids<<<ceil_div(cfg.n_traced, 256), 256, 0, s>>>(top, cfg.n_traced, trace_ids);
+      SPASM_CHECK_LAUNCH();
+    }
+    if ((r = launch_sat_keys<R>(opt_cost, cfg.m, cfg.epsilon, sk0, sv0, counters, s))) return r;
+    bool sin1 = false;
+    if ((r = launch_sort<R>(sk0, sv0, sk1, sv1, cfg.m, hist, &sin1, s))) return r;
+    const uint32_t* order = sin1 ? sv1 : sv0;
+    k_gather_chosen<R><<<cfg.p_return, 32, 0, s>>>(order, counters, cfg.p_return, opt_values, opt_cost, top, D,
+                                                   chosen_vals, out_vals, out_cost, out_idx);
+    SPASM_CHECK_LAUNCH();
+    // independent soundness re-check: fresh QUADRATIC evaluation of the chosen rows
+    if ((r = launch_evaluate<R>(m, chosen_vals, cfg.p_return, 1, recheck, s))) return r;
+    k_copy_recheck<R><<<ceil_div(cfg.p_return, 128), 128, 0, s>>>(recheck, cfg.p_return, out_recheck);
+    SPASM_CHECK_LAUNCH();
+    SPASM_CUDA_TRY(cudaMemcpyAsync(host, res, L.res_bytes, cudaMemcpyDeviceToHost, s));
+    SPASM_CUDA_TRY(cudaStreamSynchronize(s));
+
+    const unsigned int* hc = reinterpret_cast<const unsigned int*>(host);
+    const double* h_vals = reinterpret_cast<const double*>(host + 64);
+    const double* h_cost = h_vals + (size_t)cfg.p_return * D;
+    const double* h_re = h_cost + cfg.p_return;
+    const int32_t* h_idx = reinterpret_cast<const int32_t*>(h_re + cfg.p_return);
+    total_steps += per_restart;
+    {  // kernels this restart launched: sample_eval, 2 sorts (3 kernels per 8-bit pass),
+       // schedule, [trace ids], sat keys, gather, re-check evaluate, re-check copy
+      const int passes = (int)sizeof(R);
+      launches += 1 + (cfg.n > 1 ? 3 * passes : 0) + 1 + (tr && trace_ids ? 1 : 0) + 1 +
+                  (cfg.m > 1 ? 3 * passes : 0) + 3;
+    }
+    total_flagged += (int)hc[1];
+    const int n_sat = (int)hc[0];
+    if (n_sat > 0) {
+      const int k = std::min(n_sat, (int)cfg.p_return);
+      int w = 0;
+      for (int c = 0; c < k; ++c) {
+        if (!(h_re[c] < cfg.epsilon)) continue;  // chosen = chosen[recheck]
+        std::memcpy(particles + (size_t)w * D, h_vals + (size_t)c * D, (size_t)D * 8);
+        costs[w] = h_cost[c];
+        indices[w] = h_idx[c];
+        ++w;
+      }
+      rep->success = w > 0;
+      rep->restarts = restart;
+      rep->n_satisfying = n_sat;
+      rep->n_chosen = w;
+      rc = w > 0 ? SPASM_OK : SPASM_NO_SOLUTION;
+      break;
+    }
+    rep->restarts = cfg.max_restarts;
+  }
+  rep->steps = total_steps;
+  rep->launches = launches;
+  rep->flagged = total_flagged;
+  SPASM_CUDA_TRY(cudaEventRecord(e1, s));
+  SPASM_CUDA_TRY(cudaEventSynchronize(e1));
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, e0, e1);
+  rep->device_ms = ms;
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  return rc;
+}
+
+}  // namespace spasm
+
+using namespace spasm;
+
+struct spasm_model : public spasm::Model {};
+
+extern "C" {
+
+const char* spasm_last_error(void) { return spasm::last_error(); }
+int spasm_version(void) { return 1; }
+
+static int fill_bounds(Model& m, int D, const double* lower, const double* upper) {
+  SPASM_REQUIRE(D >= 1 && D <= kMaxDim, "state dimension out of range (1..128)");
+  for (int d = 0; d < D; ++d) {
+    SPASM_REQUIRE(lower[d] <= upper[d], "lower bound exceeds upper bound");
+    m.bounds.lo[d] = lower[d];
+    m.bounds.hi[d] = upper[d];
+  }
+  return SPASM_OK;
+}
+
+}  // extern "C"
+
+template <typename R>
+static void fill_tetris(TetrisScene<R>& s, int n_bodies, const int32_t* spb, const double* lc, const double* rad,
+                        int n_static, const double* sc, const double* sr, const double* sn, double wbb, double wbs,
+                        double wh, double zs, int free_yaw, const Bounds64& b, int D) {
+  std::memset(&s, 0, sizeof(s));
+  s.n_bodies = n_bodies;
+  s.n_static = n_static;
+  s.free_yaw = free_yaw ? 1 : 0;
+  s.dim = D;
+  int off = 0;
+  int uniform = n_bodies > 0 ? spb[0] : 0;
+  for (int i = 0; i < n_bodies; ++i) {
+    s.body_start[i] = off;
+    off += spb[i];
+    if (spb[i] != uniform) uniform = 0;
+  }
+  s.body_start[n_bodies] = off;
+  s.n_mov = off;
+  s.spb = (uniform == 1 || uniform == 2 || uniform == 4) ? uniform : 0;
+  for (int a = 0; a < off; ++a) {
+    s.lx[a] = (R)lc[3 * a];
+    s.ly[a] = (R)lc[3 * a + 1];
+    s.lz[a] = (R)lc[3 * a + 2];
+    s.rad[a] = (R)rad[a];
+  }
+  for (int t = 0; t < n_static; ++t) {
+    const double cx = sc[3 * t], cy = sc[3 * t + 1], cz = sc[3 * t + 2], r = sr[t];
+    const double nx = sn[3 * t], ny = sn[3 * t + 1], nz = sn[3 * t + 2];
+    s.sx[t] = (R)cx;
+    s.sy[t] = (R)cy;
+    s.sz[t] = (R)cz;
+    s.sr[t] = (R)r;
+    s.ax[t] = (R)(cx + r * nx);
+    s.ay[t] = (R)(cy + r * ny);
+    s.az[t] = (R)(cz + r * nz);
+    s.nx[t] = (R)nx;
+    s.ny[t] = (R)ny;
+    s.nz[t] = (R)nz;
+  }
+  s.w_bb = (R)wbb;
+  s.w_bs = (R)wbs;
+  s.w_h = (R)wh;
+  s.z_star = (R)zs;
+  for (int d = 0; d < D; ++d) {
+    s.lower[d] = (R)b.lo[d];
+    s.upper[d] = (R)b.hi[d];
+  }
+}
+
+extern "C" {
+
+int spasm_tetris_model_create(spasm_model** out, int n_bodies, const int32_t* spheres_per_body,
+                              const double* local_centers, const double* radii, int n_static,
+                              const double* static_centers, const double* static_radii,
+                              const double* static_normals, double w_block_block, double w_block_wall,
+                              double w_height, double z_star, int free_yaw, const double* lower,
+                              const double* upper) {
+  SPASM_REQUIRE(out != nullptr, "null output handle");
+  SPASM_REQUIRE(n_bodies >= 1 && n_bodies <= kMaxBodies, "n_bodies out of range (1..16)");
+  SPASM_REQUIRE(n_static >= 0 && n_static <= kMaxStatic, "too many static spheres (max 32)");
+  int total = 0;
+  for (int i = 0; i < n_bodies; ++i) {
+    SPASM_REQUIRE(spheres_per_body[i] >= 1, "every body needs at least one sphere");
+    total += spheres_per_body[i];
+  }
+  SPASM_REQUIRE(total <= kMaxMov, "too many movable spheres (max 128)");
+  const int D = n_bodies * (free_yaw ? 4 : 3);
+  spasm_model* m = new (std::nothrow) spasm_model();
+  SPASM_REQUIRE(m != nullptr, "out of host memory");
+  m->kind = ModelKind::Tetris;
+  m->dim = D;
+  int rc = fill_bounds(*m, D, lower, upper);
+  if (rc) {
+    delete m;
+    return rc;
+  }
+  fill_tetris<float>(m->tf, n_bodies, spheres_per_body, local_centers, radii, n_static, static_centers, static_radii,
+                     static_normals, w_block_block, w_block_wall, w_height, z_star, free_yaw, m->bounds, D);
+  fill_tetris<double>(m->td, n_bodies, spheres_per_body, local_centers, radii, n_static, static_centers,
+                      static_radii, static_normals, w_block_block, w_block_wall, w_height, z_star, free_yaw,
+                      m->bounds, D);
+  *out = m;
+  return SPASM_OK;
+}
+
+}  // extern "C"
+
+template <typename R>
+static void fill_tower(TowerScene<R>& s, int nb, double side, double half, const double* tg, int no, const double* oc,
+                       const double* orad, double ws, double wh, double wc, int free_yaw, const Bounds64& b, int D) {
+  std::memset(&s, 0, sizeof(s));
+  s.n_blocks = nb;
+  s.n_obs = no;
+  s.free_yaw = free_yaw ? 1 : 0;
+  s.dim = D;
+  s.side = (R)side;
+  s.half = (R)half;
+  s.radius = (R)(0.5 * side);
+  for (int i = 0; i < nb; ++i) s.target[i] = (R)tg[i];
+  for (int o = 0; o < no; ++o) {
+    s.ox[o] = (R)oc[3 * o];
+    s.oy[o] = (R)oc[3 * o + 1];
+    s.oz[o] = (R)oc[3 * o + 2];
+    s.orad[o] = (R)orad[o];
+  }
+  s.w_s = (R)ws;
+  s.w_h = (R)wh;
+  s.w_c = (R)wc;
+  for (int d = 0; d < D; ++d) {
+    s.lower[d] = (R)b.lo[d];
+    s.upper[d] = (R)b.hi[d];
+  }
+}
+
+extern "C" {
+
+int spasm_tower_model_create(spasm_model** out, int n_blocks, double side, double footprint_halfwidth,
+                             const double* height_targets, int n_obstacles, const double* obstacle_centers,
+                             const double* obstacle_radii, double w_stability, double w_height,
+                             double w_collision, int free_yaw, const double* lower, const double* upper) {
+  SPASM_REQUIRE(out != nullptr, "null output handle");
+  SPASM_REQUIRE(n_blocks >= 2 && n_blocks <= kMaxTowerBlocks, "n_blocks out of range (2..32)");
+  SPASM_REQUIRE(n_obstacles >= 0 && n_obstacles <= kMaxObstacles, "too many obstacles (max 64)");
+  SPASM_REQUIRE(side > 0, "cube side must be positive");
+  const int D = n_blocks * (free_yaw ? 4 : 3);
+  spasm_model* m = new (std::nothrow) spasm_model();
+  SPASM_REQUIRE(m != nullptr, "out of host memory");
+  m->kind = ModelKind::Tower;
+  m->dim = D;
+  int rc = fill_bounds(*m, D, lower, upper);
+  if (rc) {
+    delete m;
+    return rc;
+  }
+  fill_tower<float>(m->wf, n_blocks, side, footprint_halfwidth, height_targets, n_obstacles, obstacle_centers,
+                    obstacle_radii, w_stability, w_height, w_collision, free_yaw, m->bounds, D);
+  fill_tower<double>(m->wd, n_blocks, side, footprint_halfwidth, height_targets, n_obstacles, obstacle_centers,
+                     obstacle_radii, w_stability, w_height, w_collision, free_yaw, m->bounds, D);
+  *out = m;
+  return SPASM_OK;
+}
+
+void spasm_model_destroy(spasm_model* model) {
+  if (!model) return;
+  if (model->pinned) cudaFreeHost(model->pinned);
+  delete model;
+}
+
+int spasm_model_dimension(const spasm_model* model) { return model ? model->dim : -1; }
+
+#define SPASM_DTYPE_SWITCH(dtype, ...)                          \
+  do {                                                          \
+    if ((dtype) == SPASM_F32) {                                 \
+      using R = float;                                          \
+      __VA_ARGS__                                               \
+    } else if ((dtype) == SPASM_F64) {                          \
+      using R = double;                                         \
+      __VA_ARGS__                                               \
+    } else {                                                    \
+      spasm::set_last_error("dtype must be SPASM_F32 or SPASM_F64"); \
+      return SPASM_ERR_USAGE;                                   \
+    }                                                           \
+  } while (0)
+
+int spasm_evaluate(const spasm_model* model, int dtype, const void* values, int64_t P, int mode, void* costs,
+                   void* stream) {
+  SPASM_REQUIRE(model != nullptr, "null model");
+  SPASM_REQUIRE(mode == SPASM_LINEAR || mode == SPASM_QUADRATIC, "unknown cost mode");
+  SPASM_DTYPE_SWITCH(dtype, return launch_evaluate<R>(*model, static_cast<const R*>(values), P, mode,
+                                                      static_cast<R*>(costs), as_stream(stream)););
+}
+
+int spasm_gradient(const spasm_model* model, int dtype, const void* values, int64_t P, int mode, void* grad,
+                   void* stream) {
+  SPASM_REQUIRE(model != nullptr, "null model");
+  SPASM_REQUIRE(mode == SPASM_LINEAR || mode == SPASM_QUADRATIC, "unknown cost mode");
+  SPASM_DTYPE_SWITCH(dtype, return launch_gradient<R>(*model, static_cast<const R*>(values), P, mode,
+                                                      static_cast<R*>(grad), as_stream(stream)););
+}
+
+int spasm_pcg64_state(uint64_t seed, uint64_t restart, uint64_t out[4]) {
+  SPASM_REQUIRE(out != nullptr, "null output");
+  seedseq_pcg64(seed, &restart, 1, out);
+  return SPASM_OK;
+}
+
+int spasm_sample(int dtype, int D, const double* lower, const double* upper, uint64_t seed, uint64_t restart,
+                 int sampler, int64_t row_offset, int64_t N, const double* warm_dev, int64_t n_warm, void* values,
+                 void* stream) {
+  SPASM_REQUIRE(D >= 1 && D <= kMaxDim, "state dimension out of range (1..128)");
+  SPASM_REQUIRE(N >= 0 && row_offset >= 0, "negative row range");
+  Bounds64 b;
+  for (int d = 0; d < D; ++d) {
+    b.lo[d] = lower[d];
+    b.hi[d] = upper[d];
+  }
+  const Pcg64State st = restart_state(seed, restart);
+  SPASM_DTYPE_SWITCH(dtype, return launch_sample<R>(b, D, st, row_offset, N, warm_dev, n_warm, sampler, seed,
+                                                    (uint32_t)restart, static_cast<R*>(values), as_stream(stream)););
+}
+
+int spasm_sample_eval(const spasm_model* model, int dtype, uint64_t seed, uint64_t restart, int sampler,
+                      int64_t row_offset, int64_t N, const double* warm_dev, int64_t n_warm, void* values, void* keys,
+                      uint32_t* idx, void* stream) {
+  SPASM_REQUIRE(model != nullptr, "null model");
+  SPASM_REQUIRE(N >= 0 && row_offset >= 0, "negative row range");
+  const Pcg64State st = restart_state(seed, restart);
+  SPASM_DTYPE_SWITCH(dtype, return launch_sample_eval<R>(*model, st, row_offset, N, warm_dev, n_warm, sampler, seed,
+                                                         (uint32_t)restart, static_cast<R*>(values),
+                                                         static_cast<typename KeyOf<R>::type*>(keys), idx,
+                                                         as_stream(stream)););
+}
+
+int spasm_step(int dtype, void* values, const void* grad, int64_t P, int D, double rate, const void* lower,
+               const void* upper, uint8_t* flagged, void* stream) {
+  SPASM_REQUIRE(rate >= 0, "rate must be >= 0");
+  SPASM_DTYPE_SWITCH(dtype, return launch_step<R>(static_cast<R*>(values), static_cast<const R*>(grad), P, D, (R)rate,
+                                                  static_cast<const R*>(lower), static_cast<const R*>(upper), flagged,
+                                                  as_stream(stream)););
+}
+
+int spasm_descent_schedule(const spasm_model* model, int dtype, const void* src, const uint32_t* rows, int64_t M,
+                           int k_lin, int k_quad, double eta_init, double alpha, double epsilon, void* out_values,
+                           void* out_cost, uint8_t* flagged, uint32_t* flagged_count, void* trace_cost,
+                           uint8_t* trace_sat, int n_traced, void* stream) {
+  SPASM_REQUIRE(model != nullptr, "null model");
+  SPASM_REQUIRE(k_lin >= 0 && k_quad >= 0, "step counts must be nonnegative");
+  SPASM_DTYPE_SWITCH(dtype, return launch_schedule<R>(*model, static_cast<const R*>(src), rows, M, k_lin, k_quad,
+                                                      eta_init, alpha, epsilon, static_cast<R*>(out_values),
+                                                      static_cast<R*>(out_cost), flagged, flagged_count,
+                                                      static_cast<R*>(trace_cost), trace_sat, n_traced,
+                                                      as_stream(stream)););
+}
+
+int64_t spasm_sort_workspace_bytes(int dtype, int64_t n) {
+  const int64_t ksz = dtype == SPASM_F64 ? 8 : 4;
+  const int64_t tiles = (n + 2047) / 2048 + 1;
+  return align_up((size_t)(n * ksz)) + align_up((size_t)(n * 4)) + align_up((size_t)(tiles * 256 * 4));
+}
+
+int spasm_sort_pairs(int dtype, void* keys, uint32_t* vals, int64_t n, void* workspace, void* stream) {
+  SPASM_REQUIRE(n >= 0 && n <= (int64_t)0xFFFFFFFF, "sort size out of range");
+  if (n <= 1) return SPASM_OK;
+  SPASM_REQUIRE(workspace != nullptr, "null sort workspace");
+  const int64_t ksz = dtype == SPASM_F64 ? 8 : 4;
+  char* w = static_cast<char*>(workspace);
+  void* k1 = w;
+  uint32_t* v1 = reinterpret_cast<uint32_t*>(w + align_up((size_t)(n * ksz)));
+  unsigned int* hist = reinterpret_cast<unsigned int*>(w + align_up((size_t)(n * ksz)) + align_up((size_t)(n * 4)));
+  cudaStream_t s = as_stream(stream);
+  SPASM_DTYPE_SWITCH(dtype, {
+    using K = typename KeyOf<R>::type;
+    bool in1 = false;
+    int r = launch_sort<R>(static_cast<K*>(keys), vals, static_cast<K*>(k1), v1, n, hist, &in1, s);
+    if (r) return r;
+    if (in1) {
+      SPASM_CUDA_TRY(cudaMemcpyAsync(keys, k1, (size_t)(n * ksz), cudaMemcpyDeviceToDevice, s));
+      SPASM_CUDA_TRY(cudaMemcpyAsync(vals, v1, (size_t)(n * 4), cudaMemcpyDeviceToDevice, s));
+    }
+    return SPASM_OK;
+  });
+}
+
+int spasm_cost_keys(int dtype, const void* costs, int64_t P, double threshold, void* keys, uint32_t* vals,
+                    uint32_t* n_below, void* stream) {
+  SPASM_REQUIRE(P >= 0, "negative size");
+  SPASM_DTYPE_SWITCH(dtype, {
+    using K = typename KeyOf<R>::type;
+    return launch_sat_keys<R>(static_cast<const R*>(costs), P, threshold, static_cast<K*>(keys), vals,
+                              reinterpret_cast<unsigned int*>(n_below), as_stream(stream));
+  });
+}
+
+int64_t spasm_solve_workspace_bytes(const spasm_model* model, int dtype, const spasm_solve_config* cfg,
+                                    int64_t n_warm) {
+  if (!model || !cfg) return -1;
+  if (dtype == SPASM_F64) return (int64_t)make_layout<double>(model->dim, *cfg, n_warm).total;
+  return (int64_t)make_layout<float>(model->dim, *cfg, n_warm).total;
+}
+
+int spasm_solve(const spasm_model* model, int dtype, const spasm_solve_config* cfg, const double* warm_host,
+                int64_t n_warm, void* workspace, int64_t workspace_bytes, double* particles, double* costs,
+                int64_t* indices, spasm_solve_report* report, void* trace_cost, uint8_t* trace_sat,
+                int32_t* trace_ids, void* stream) {
+  SPASM_REQUIRE(model != nullptr, "null model");
+  int r = validate_cfg(cfg);
+  if (r) return r;
+  SPASM_REQUIRE(particles && costs && indices && report, "null output buffer");
+  Model& m = const_cast<spasm_model&>(*model);
+  SPASM_DTYPE_SWITCH(dtype, return solve_impl<R>(m, *cfg, warm_host, n_warm, workspace, workspace_bytes, particles,
+                                                 costs, indices, report, static_cast<R*>(trace_cost), trace_sat,
+                                                 trace_ids, as_stream(stream)););
+}
+
+}  // extern "C"

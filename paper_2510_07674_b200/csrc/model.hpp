@@ -1,0 +1,31 @@
+// Host-side model object behind the opaque spasm_model handle.
+#pragma once
+#include "scene.cuh"
+
+namespace spasm {
+
+enum class ModelKind { Tetris = 1, Tower = 2 };
+
+struct Model {
+  ModelKind kind;
+  int dim;
+  TetrisScene<float> tf;
+  TetrisScene<double> td;
+  TowerScene<float> wf;
+  TowerScene<double> wd;
+  // double-precision bounds for the bit-exact sampler (numpy draws in float64)
+  Bounds64 bounds;
+  // pinned staging for solve results (grown on demand, never inside a kernel sequence)
+  void* pinned = nullptr;
+  size_t pinned_bytes = 0;
+
+  template <typename R> const TetrisScene<R>& tetris() const;
+  template <typename R> const TowerScene<R>& tower() const;
+};
+
+template <> inline const TetrisScene<float>& Model::tetris<float>() const { return tf; }
+template <> inline const TetrisScene<double>& Model::tetris<double>() const { return td; }
+template <> inline const TowerScene<float>& Model::tower<float>() const { return wf; }
+template <> inline const TowerScene<double>& Model::tower<double>() const { return wd; }
+
+}  // namespace spasm

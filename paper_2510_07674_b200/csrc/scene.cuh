@@ -1,0 +1,61 @@
+// Device-resident scene tables for the stage-1 placement cost models.
+//
+// These are POD structs passed BY VALUE as kernel parameters: every table read in
+// the pair loops is warp-uniform, so it is served from the constant bank (LDC /
+// direct c[0x0][..] operands) with no shared-memory traffic and no divergence.
+//
+//   TetrisScene  <- SphereInteractions tables + TetrisCostModel terms
+//                   (reference problems/_interactions.py:23-93, problems/tetris.py:159-245)
+//   TowerScene   <- TowerCostModel terms (reference problems/tower.py:144-322)
+#pragma once
+#include "common.cuh"
+
+namespace spasm {
+
+constexpr int kMaxBodies = 16;    // movable bodies (blocks) per tetris scene
+constexpr int kMaxMov = 128;      // movable spheres in total
+constexpr int kMaxStatic = 32;    // static spheres (walls)
+constexpr int kMaxDim = 128;      // particle state dimension D
+constexpr int kMaxTowerBlocks = 32;
+constexpr int kMaxObstacles = 64;
+
+// float64 clamp/sampling bounds (numpy draws and clamps warm seeds in float64)
+struct Bounds64 {
+  double lo[kMaxDim];
+  double hi[kMaxDim];
+};
+
+template <typename R>
+struct TetrisScene {
+  int n_bodies;                     // n
+  int n_mov;                        // S_mov
+  int n_static;                     // walls
+  int free_yaw;                     // row layout (x,y,z,yaw) per block if 1 else (x,y,z)
+  int dim;                          // n * (3 + free_yaw)
+  int spb;                          // spheres per body if uniform, else 0
+  int body_start[kMaxBodies + 1];   // sphere index range per body (C order, tetris.py:203-210)
+  R lx[kMaxMov], ly[kMaxMov], lz[kMaxMov], rad[kMaxMov];  // body-local centres, radii
+  // static spheres: centre + radius (fp64 path, identical to numpy's form) and the
+  // cancellation-free anchor form used by the fp32 path: tangent point a = s + R n
+  // and unit normal n, so |c-s|^2 - R^2 = |v|^2 + 2R v.n with v = c - a small.
+  R sx[kMaxStatic], sy[kMaxStatic], sz[kMaxStatic], sr[kMaxStatic];
+  R ax[kMaxStatic], ay[kMaxStatic], az[kMaxStatic];
+  R nx[kMaxStatic], ny[kMaxStatic], nz[kMaxStatic];
+  R w_bb, w_bs, w_h, z_star;        // PackingWeights + packing plane
+  R lower[kMaxDim], upper[kMaxDim]; // clamp box (tetris.py:174-187)
+};
+
+template <typename R>
+struct TowerScene {
+  int n_blocks;                     // B (>= 2)
+  int n_obs;                        // O
+  int free_yaw;
+  int dim;
+  R side, half, radius;             // cube edge, footprint half-width, inscribed sphere radius
+  R target[kMaxTowerBlocks];        // (i+1)*side (tower.py:100-102)
+  R ox[kMaxObstacles], oy[kMaxObstacles], oz[kMaxObstacles], orad[kMaxObstacles];
+  R w_s, w_h, w_c;                  // TowerWeights
+  R lower[kMaxDim], upper[kMaxDim];
+};
+
+}  // namespace spasm

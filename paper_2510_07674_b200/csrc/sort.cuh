@@ -1,0 +1,130 @@
+// Stable device-wide LSD radix sort of (key, uint32 value) pairs, 8-bit digits.
+//
+// Replaces np.argsort(costs, kind="stable") in select_topk and in the final
+// satisfying-particle ordering (reference particle_opt.py:195-200 and :363). Keys are
+// order-preserving images of the IEEE costs (common.cuh order_key), values are row
+// indices in ascending order, and every pass is stable, so ties resolve by index
+// exactly like numpy's stable sort.
+//
+// Per pass: k_radix_hist (per-tile digit histogram, digit-major) -> k_radix_scan
+// (exclusive scan over digit x tile) -> k_radix_scatter (stable in-tile ranking with
+// __match_any_sync + per-warp digit counters, then scatter).
+#pragma once
+#include "common.cuh"
+
+namespace spasm {
+
+constexpr int kSortThreads = 256;
+constexpr int kSortItems = 8;  // per thread per tile
+constexpr int kSortTile = kSortThreads * kSortItems;
+constexpr int kSortWarps = kSortThreads / 32;
+
+template <typename K>
+__global__ void __launch_bounds__(kSortThreads) k_radix_hist(const K* __restrict__ keys, int64_t n, int shift,
+                                                             unsigned int* __restrict__ hist, int nblocks) {
+  __shared__ unsigned int h[256];
+  h[threadIdx.x] = 0;
+  __syncthreads();
+  const int64_t base = (int64_t)blockIdx.x * kSortTile;
+#pragma unroll
+  for (int r = 0; r < kSortItems; ++r) {
+    const int64_t i = base + r * kSortThreads + threadIdx.x;
+    if (i < n) atomicAdd(&h[(unsigned)((keys[i] >> shift) & 0xFF)], 1u);
+  }
+  __syncthreads();
+  hist[(int64_t)threadIdx.x * nblocks + blockIdx.x] = h[threadIdx.x];
+}
+
+// Exclusive scan of `total` counters by one CTA of 1024 threads.
+static __global__ void __launch_bounds__(1024) k_radix_scan(unsigned int* __restrict__ hist, int64_t total) {
+  __shared__ unsigned int part[1024];
+  const int64_t chunk = (total + 1023) / 1024;
+  const int64_t b = threadIdx.x * chunk, e = min(total, b + chunk);
+  unsigned int s = 0;
+  for (int64_t i = b; i < e; ++i) s += hist[i];
+  part[threadIdx.x] = s;
+  __syncthreads();
+  for (int off = 1; off < 1024; off <<= 1) {
+    unsigned int v = threadIdx.x >= off ? part[threadIdx.x - off] : 0;
+    __syncthreads();
+    part[threadIdx.x] += v;
+    __syncthreads();
+  }
+  unsigned int acc = part[threadIdx.x] - s;
+  for (int64_t i = b; i < e; ++i) {
+    const unsigned int v = hist[i];
+    hist[i] = acc;
+    acc += v;
+  }
+}
+
+template <typename K>
+__global__ void __launch_bounds__(kSortThreads) k_radix_scatter(const K* __restrict__ kin, const uint32_t* __restrict__ vin,
+                                                                K* __restrict__ kout, uint32_t* __restrict__ vout,
+                                                                int64_t n, int shift,
+                                                                const unsigned int* __restrict__ hist, int nblocks) {
+  __shared__ unsigned int running[256];
+  __shared__ unsigned int wcnt[kSortWarps][256];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  running[threadIdx.x] = hist[(int64_t)threadIdx.x * nblocks + blockIdx.x];
+  for (int w = 0; w < kSortWarps; ++w) wcnt[w][threadIdx.x] = 0;
+  __syncthreads();
+  const int64_t base = (int64_t)blockIdx.x * kSortTile;
+  const unsigned lt_mask = (1u << lane) - 1u;
+  for (int r = 0; r < kSortItems; ++r) {
+    const int64_t i = base + r * kSortThreads + threadIdx.x;
+    const bool valid = i < n;
+    K key = valid ? kin[i] : K(0);
+    uint32_t val = valid ? vin[i] : 0u;
+    const unsigned digit = valid ? (unsigned)((key >> shift) & 0xFF) : 256u;
+    const unsigned peers = __match_any_sync(0xFFFFFFFFu, digit);
+    const unsigned rank = __popc(peers & lt_mask);
+    const bool leader = rank == 0;
+    if (valid && leader) wcnt[warp][digit] = __popc(peers);
+    __syncthreads();
+    {  // exclusive prefix over warps for digit = threadIdx.x, seeded by the running offset
+      unsigned acc = running[threadIdx.x];
+#pragma unroll
+      for (int w = 0; w < kSortWarps; ++w) {
+        const unsigned t = wcnt[w][threadIdx.x];
+        wcnt[w][threadIdx.x] = acc;
+        acc += t;
+      }
+      running[threadIdx.x] = acc;
+    }
+    __syncthreads();
+    if (valid) {
+      const unsigned pos = wcnt[warp][digit] + rank;
+      kout[pos] = key;
+      vout[pos] = val;
+    }
+    __syncthreads();
+    for (int w = 0; w < kSortWarps; ++w) wcnt[w][threadIdx.x] = 0;
+    __syncthreads();
+  }
+}
+
+// Host driver. Sorts (k0, v0) by key bits [0, key_bits) into (k1, v1) ping-pong
+// buffers; returns through *result_in_1 whether the final data sits in k1/v1.
+// hist must hold 256 * ceil(n / kSortTile) counters.
+template <typename K>
+inline cudaError_t radix_sort_pairs(K* k0, uint32_t* v0, K* k1, uint32_t* v1, int64_t n, int key_bits,
+                                    unsigned int* hist, bool* result_in_1, cudaStream_t stream) {
+  *result_in_1 = false;
+  if (n <= 1) return cudaSuccess;
+  const int nblocks = ceil_div(n, kSortTile);
+  K* ka = k0; K* kb = k1; uint32_t* va = v0; uint32_t* vb = v1;
+  bool in1 = false;
+  for (int shift = 0; shift < key_bits; shift += 8) {
+    k_radix_hist<K><<<nblocks, kSortThreads, 0, stream>>>(ka, n, shift, hist, nblocks);
+    k_radix_scan<<<1, 1024, 0, stream>>>(hist, (int64_t)256 * nblocks);
+    k_radix_scatter<K><<<nblocks, kSortThreads, 0, stream>>>(ka, va, kb, vb, n, shift, hist, nblocks);
+    std::swap(ka, kb);
+    std::swap(va, vb);
+    in1 = !in1;
+  }
+  *result_in_1 = in1;
+  return cudaGetLastError();
+}
+
+}  // namespace spasm

@@ -1,0 +1,77 @@
+"""The C-ABI library loads, exports every symbol include/spasm.h declares, and its
+host-only entry points behave (no GPU needed: no compute calls here)."""
+from __future__ import annotations
+
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+from conftest import ROOT
+from paper_2510_07674_b200 import _native as nat
+
+
+def declared_functions():
+    names = set()
+    for h in os.listdir(os.path.join(ROOT, "include")):
+        if h.endswith(".h"):
+            src = open(os.path.join(ROOT, "include", h)).read()
+            names |= set(re.findall(r"\b(spasm_[a-z0-9_]+)\s*\(", src))
+    return sorted(names)
+
+
+def test_library_exports_every_declared_symbol():
+    lib = nat.load()
+    names = declared_functions()
+    assert len(names) >= 15
+    for n in names:
+        assert hasattr(lib, n), n
+    # the ctypes signature table covers the whole header
+    assert set(names) <= set(nat.SIGNATURES)
+
+
+@pytest.mark.parametrize("seed,restart", [(0, 0), (0, 1), (12345, 7), (2**40 + 3, 1 << 20), (99, 63)])
+def test_seedsequence_restatement_matches_numpy(seed, restart):
+    out = (ctypes.c_uint64 * 4)()
+    assert nat.load().spasm_pcg64_state(seed, restart, out) == 0
+    st = np.random.PCG64(np.random.SeedSequence(entropy=seed, spawn_key=(restart,))).state["state"]
+    assert (out[0] << 64) | out[1] == st["state"]
+    assert (out[2] << 64) | out[3] == st["inc"]
+
+
+def test_model_create_rejects_bad_input():
+    lib = nat.load()
+    h = ctypes.c_void_p()
+    spb = np.array([1], dtype=np.int32)
+    c = np.zeros((1, 3))
+    r = np.ones(1)
+    lo = np.array([1.0, 0.0, 0.0])
+    hi = np.array([0.0, 1.0, 1.0])  # lower > upper
+    st = lib.spasm_tetris_model_create(ctypes.byref(h), 1, nat.ptr(spb), nat.ptr(c), nat.ptr(r), 0, None, None, None,
+                                       1.0, 1.0, 1.0, 0.0, 0, nat.ptr(lo), nat.ptr(hi))
+    assert st == nat.SPASM_ERR_USAGE
+    assert "lower bound" in nat.last_error()
+    with pytest.raises(ValueError):
+        nat.check(st, "create")
+
+
+def test_model_dimension_and_destroy():
+    from paper_2510_07674_b200.problems import as_cost_model, load_scene
+
+    for name, d in (("tetris5", 15), ("tetris8", 24), ("tower4", 12), ("domino2", 6)):
+        m = as_cost_model(load_scene(name).problem)
+        assert nat.load().spasm_model_dimension(m.handle) == d == m.dimension
+
+
+def test_no_cpu_fallback_without_gpu():
+    import torch
+
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    from paper_2510_07674_b200.problems import as_cost_model, load_scene
+
+    m = as_cost_model(load_scene("tetris5").problem)
+    with pytest.raises(nat.NativeError):
+        m.evaluate(np.zeros((2, 15)), "linear")
