@@ -90,13 +90,17 @@ class PairTable:
         d = np.sqrt(np.sum(diff * diff, axis=-1))
         return diff, d, drot
 
-    def margin(self, pos, yaw):
+    def margin(self, pos, yaw, static_band=1e-2):
         """Per row, the smallest |rsum - d| over all entries: distance to a hinge kink
-        (where fp32 and fp64 may legitimately disagree on the active set)."""
+        (where fp32 and fp64 may legitimately disagree on the active set). Static (wall)
+        entries are scaled by 1/static_band: the fp32 kernel evaluates them in an exact
+        cancellation-free form whose error is ~1e-8, so their kink band is ~100x narrower."""
         if len(self.a) == 0:
             return np.full(pos.shape[0], np.inf)
         _, d, _ = self._diff(pos, yaw)
-        return np.min(np.abs(self.rsum - d), axis=1)
+        gap = np.abs(self.rsum - d)
+        gap = np.where(self.b_mov[None, :], gap, gap / static_band)
+        return np.min(gap, axis=1)
 
     def cost(self, pos, yaw, mode):
         if len(self.a) == 0:

@@ -18,14 +18,19 @@
 
 namespace spasm {
 
-// --- one sphere pair: returns pen; accumulates the gradient on sphere a ----------
+// --- one sphere pair ---------------------------------------------------------------
+// Adds the UNWEIGHTED pen (or pen^2) to `cost` and returns the unweighted gradient
+// scale s with d cost / d ca = -w * s * (ca - cb) (linear: s = 1/d, quadratic: s = 2 pen/d,
+// 0 when inactive). Callers apply the group weight once per body pair.
+//   fp32: one MUFU.RSQ per pair (d = d2 * rs, 1/d = rs). In the gradient-only path the
+//   d2 clamp is dropped: d2 == 0 gives rs = inf, d = NaN, pen > 0 false -> inactive,
+//   exactly the reference's "coincident centres contribute zero" rule.
 template <typename R, bool WC, bool WG, bool Q>
-__device__ __forceinline__ void pen_pair_acc(R dx, R dy, R dz, R rsum, R w, R& cost,
-                                             R& gx, R& gy, R& gz) {
+__device__ __forceinline__ R pair_scale(R dx, R dy, R dz, R rsum, R& cost) {
   const R d2 = dx * dx + dy * dy + dz * dz;
   R d, inv;
   if constexpr (sizeof(R) == 4) {
-    inv = Math<R>::rsqrt_pos(d2);
+    inv = WC ? rsqrtf(fmaxf(d2, 1e-30f)) : rsqrtf(d2);
     d = d2 * inv;
   } else {
     d = sqrt(d2);
@@ -34,15 +39,26 @@ __device__ __forceinline__ void pen_pair_acc(R dx, R dy, R dz, R rsum, R w, R& c
   const R pen = rsum - d;
   if constexpr (WC) {
     const R pc = pen > R(0) ? pen : R(0);
-    cost += Q ? w * (pc * pc) : w * pc;
+    cost += Q ? pc * pc : pc;
   }
   if constexpr (WG) {
-    const bool active = (pen > R(0)) && (d2 > R(0));
-    const R f = Q ? R(2) * w * pen : w;
-    const R s = active ? -f * inv : R(0);
-    gx += s * dx;
-    gy += s * dy;
-    gz += s * dz;
+    if constexpr (sizeof(R) == 4) return pen > R(0) ? (Q ? R(2) * pen * inv : inv) : R(0);
+    else return (pen > R(0) && d2 > R(0)) ? (Q ? R(2) * pen * inv : inv) : R(0);
+  }
+  return R(0);
+}
+
+// weighted form (tower / generic callers): accumulates g = d cost / d ca
+template <typename R, bool WC, bool WG, bool Q>
+__device__ __forceinline__ void pen_pair_acc(R dx, R dy, R dz, R rsum, R w, R& cost, R& gx, R& gy, R& gz) {
+  R c = R(0);
+  const R s = pair_scale<R, WC, WG, Q>(dx, dy, dz, rsum, c);
+  if constexpr (WC) cost += w * c;
+  if constexpr (WG) {
+    const R ws = -w * s;
+    gx += ws * dx;
+    gy += ws * dy;
+    gz += ws * dz;
   }
 }
 
@@ -64,7 +80,7 @@ __device__ __forceinline__ void pen_static_acc(const TetrisScene<R>& sc, int st,
     const R d2 = Rs * Rs + q;
     const R inv = Math<R>::rsqrt_pos(d2);
     const R d = d2 * inv;
-    const R pen = rc - q / (d + Rs);
+    const R pen = rc - __fdividef(q, d + Rs);
     if constexpr (WC) {
       const R pc = pen > R(0) ? pen : R(0);
       cost += Q ? w * (pc * pc) : w * pc;
@@ -128,7 +144,7 @@ struct TetrisEval {
         }
         const int b0 = sc.body_start[j];
         const int nb = SPB ? SPB : sc.body_start[j + 1] - b0;
-        R gpx = R(0), gpy = R(0), gpz = R(0), gyi = R(0), gyj = R(0);
+        R gpx = R(0), gpy = R(0), gpz = R(0), gyi = R(0), gyj = R(0), cpair = R(0);
         if constexpr (SPB > 0) {
           // preload body j's world spheres into registers
           R wbx[SPB], wby[SPB], wbz[SPB], rbx_[SPB], rby_[SPB], rb[SPB];
@@ -161,16 +177,15 @@ struct TetrisEval {
             const R ra = sc.rad[a];
 #pragma unroll
             for (int sb = 0; sb < SPB; ++sb) {
-              R gx = R(0), gy = R(0), gz = R(0);
-              pen_pair_acc<R, WC, WG, Q>(wax - wbx[sb], way - wby[sb], waz - wbz[sb], ra + rb[sb],
-                                         sc.w_bb, cost, gx, gy, gz);
+              const R dx = wax - wbx[sb], dy = way - wby[sb], dz = waz - wbz[sb];
+              const R s = pair_scale<R, WC, WG, Q>(dx, dy, dz, ra + rb[sb], cpair);
               if constexpr (WG) {
-                gpx += gx;
-                gpy += gy;
-                gpz += gz;
+                gpx += s * dx;
+                gpy += s * dy;
+                gpz += s * dz;
                 if constexpr (FREE) {
-                  gyi += gy * rx - gx * ry;
-                  gyj += gy * rbx_[sb] - gx * rby_[sb];
+                  gyi += s * (dy * rx - dx * ry);
+                  gyj += s * (dy * rbx_[sb] - dx * rby_[sb]);
                 }
               }
             }
@@ -194,22 +209,28 @@ struct TetrisEval {
                 uy = sj * ux + cj * uy;
                 ux = t;
               }
-              R gx = R(0), gy = R(0), gz = R(0);
-              pen_pair_acc<R, WC, WG, Q>(wax - (pjx + ux), way - (pjy + uy), waz - (pjz + sc.lz[b]),
-                                         ra + sc.rad[b], sc.w_bb, cost, gx, gy, gz);
+              const R dx = wax - (pjx + ux), dy = way - (pjy + uy), dz = waz - (pjz + sc.lz[b]);
+              const R s = pair_scale<R, WC, WG, Q>(dx, dy, dz, ra + sc.rad[b], cpair);
               if constexpr (WG) {
-                gpx += gx;
-                gpy += gy;
-                gpz += gz;
+                gpx += s * dx;
+                gpy += s * dy;
+                gpz += s * dz;
                 if constexpr (FREE) {
-                  gyi += gy * rx - gx * ry;
-                  gyj += gy * ux - gx * uy;
+                  gyi += s * (dy * rx - dx * ry);
+                  gyj += s * (dy * ux - dx * uy);
                 }
               }
             }
           }
         }
+        if constexpr (WC) cost += sc.w_bb * cpair;
         if constexpr (WG) {
+          const R wneg = -sc.w_bb;  // group weight applied once per body pair
+          gpx *= wneg;
+          gpy *= wneg;
+          gpz *= wneg;
+          gyi *= wneg;
+          gyj *= wneg;
           gix += gpx;
           giy += gpy;
           giz += gpz;
