@@ -156,6 +156,117 @@ int spasm_solve(const spasm_model* model, int dtype, const spasm_solve_config* c
                 int64_t* indices, spasm_solve_report* report, void* trace_cost, uint8_t* trace_sat,
                 int32_t* trace_ids, void* stream);
 
+
+/* =====================================================================================
+ * Stage 2: trajectory optimization (reference trajopt.py / robot.py)
+ * ===================================================================================== */
+typedef struct spasm_traj spasm_traj; /* opaque: one problem's _Geometry (trajopt.py:235-367) */
+
+/* KinematicChain (robot.py:45-68) + its flattened link-sphere table (trajopt.py:311-321). */
+typedef struct {
+  int32_t dof, n_spheres;
+  const double* axes;             /* dof*3 unit joint axes in the body frame */
+  const double* offsets;          /* dof*3 translation applied before each joint */
+  const double* lower;            /* dof joint limits */
+  const double* upper;
+  const double* tool_translation; /* 3 */
+  const double* tool_rotation;    /* 9, row-major */
+  const double* sphere_centers;   /* n_spheres*3 link-frame centres, sorted by link */
+  const double* sphere_radii;     /* n_spheres */
+  const int32_t* sphere_link;     /* n_spheres owning joint index (ascending) */
+} spasm_chain;
+
+/* Problem side of _build_geometry (trajopt.py:305-367). */
+typedef struct {
+  int32_t manipulation;           /* 0 = point-to-point MotionProblem (problems/motion.py) */
+  int32_t n_blocks;               /* segments, skeleton order */
+  const int32_t* spheres_per_block;
+  const double* block_centers;    /* object-frame sphere centres (sum spheres_per_block)*3 */
+  const double* block_radii;
+  const double* staged_poses;     /* n_blocks*4 (x, y, z, yaw): problem.initial_poses */
+  const double* grasp_offset;     /* GraspSpec.offset (3) */
+  double grasp_yaw_offset;        /* GraspSpec.yaw_offset */
+  int32_t n_static;
+  const double* static_centers;   /* n_static*3 */
+  const double* static_radii;
+  const spasm_model* place_model; /* free-yaw placement twin (trajopt.py:281-302); NULL for motion */
+  int32_t anchor_yaw;             /* problem.yaw_mode == fixed */
+  int32_t rows_have_yaw;          /* stage-1 rows are (x, y, z, yaw) per block */
+  const double* start;            /* motion endpoints (dof each) */
+  const double* goal;
+} spasm_traj_desc;
+
+int spasm_traj_create(spasm_traj** out, const spasm_chain* chain, const spasm_traj_desc* desc);
+void spasm_traj_destroy(spasm_traj* traj);
+int spasm_traj_segments(const spasm_traj* traj);
+
+/* TrajOptConfig (trajopt.py:118-177); waypoints = k_interp*(k_waypoint+1)+1. */
+typedef struct {
+  double w_start, w_arm, w_block, w_place, mu0, beta, lr_init, lr_final, validation_epsilon;
+  int32_t outer_iters, inner_steps;
+  int32_t place_mode;             /* placement-term mode used inside solve_al */
+  int32_t waypoints;
+} spasm_al_config;
+
+typedef struct {
+  int32_t status;                 /* SPASM_OK, SPASM_AL_FAILURE or SPASM_LIFT_FAILURE */
+  int32_t accepted_outer;         /* outer iteration of the accepted particle (-1 on failure) */
+  int32_t particle_index;         /* AlResult.particle_index */
+  int32_t n_outers;               /* OuterRecords in the report */
+  int32_t n_particles;            /* particles in the batch (after lifting) */
+  int32_t lift_pick_fail;         /* first unreachable staged pose, -1 if none */
+  double objective;               /* AlResult.objective */
+  double least_violation;         /* TrajOptFailure.best_violation */
+  double device_ms;
+} spasm_al_result;
+
+/* fk_batch (+ yaw_jacobian_batch) (robot.py:160-224). Q (n,dof) device; ee (n,3), rot (n,9);
+ * origins/axes (n,dof,3) and yaw_jacobian (n,dof) optional (NULL). */
+int spasm_fk(const spasm_traj* traj, int dtype, const void* Q, int64_t n, void* ee, void* rot, void* origins,
+             void* axes, void* yaw_jacobian, void* stream);
+/* ik_solve_batch (robot.py:227-302): per target, `restarts` seeds from
+ * SeedSequence(seed, spawn_key=(target,)); targets are float64 device arrays. */
+int spasm_ik_solve(const spasm_traj* traj, int dtype, const double* target_pos, const double* target_yaw,
+                   int64_t n_targets, uint64_t seed, int restarts, int max_iters, double damping, void* solutions,
+                   uint8_t* success, void* errors, void* stream);
+/* _polish_tool_down (trajopt.py:726-776), in place on Q (n,dof). */
+int spasm_polish_tool_down(const spasm_traj* traj, int dtype, void* Q, const double* target_pos,
+                           const double* target_yaw, int64_t n, uint8_t* ok, void* stream);
+/* _evaluate (trajopt.py:416-653): values (P,B,T,dof); lam (P,3), mu (P) may be NULL (zero).
+ * Outputs objective (P), constraints (P,3), lagrangian (P), grad (P,B,T,dof) (each optional). */
+int spasm_traj_evaluate(const spasm_traj* traj, int dtype, const spasm_al_config* cfg, const void* values,
+                        int64_t P, int mode, int place_mode, const void* lam, const void* mu, int want_grad,
+                        void* objective, void* constraints, void* lagrangian, void* grad, void* stream);
+/* validate (trajopt.py:1071-1153) for P trajectories. */
+int spasm_traj_validate(const spasm_traj* traj, int dtype, const spasm_al_config* cfg, const void* values,
+                        int64_t P, uint8_t* feasible, void* violation, void* stream);
+/* lift_placements (trajopt.py:795-876), asynchronous: placements (P,D) float64 device rows.
+ * Writes endpoints (kept,B,2,dof), kept[] row indices and status[2] = {first unreachable
+ * staged pose or -1, kept count} on the device. */
+int64_t spasm_lift_workspace_bytes(const spasm_traj* traj, int dtype, int64_t P, int candidates);
+int spasm_lift(const spasm_traj* traj, int dtype, const double* placements, int64_t P, int D, uint64_t seed,
+               int candidates, void* workspace, int64_t workspace_bytes, void* endpoints, int32_t* kept,
+               int32_t* status, void* stream);
+/* init_trajectories (trajopt.py:892-923) from a PCG64 state (the Generator the caller passes);
+ * n_active (device, optional) bounds the live rows. spasm_trajectory_stream_state gives the
+ * state of SeedSequence(seed, spawn_key=(1<<20,)) (bench.py:88-91). */
+int spasm_trajectory_stream_state(uint64_t seed, uint64_t out[4]);
+int spasm_init_trajectories(const spasm_traj* traj, int dtype, const void* endpoints, int64_t P, int n_segments,
+                            const int32_t* n_active, int k_waypoint, int k_interp, const uint64_t pcg_state[4],
+                            void* out, void* stream);
+/* solve_al (trajopt.py:936-1063) as one persistent launch. Synchronous: returns
+ * SPASM_OK / SPASM_AL_FAILURE / SPASM_LIFT_FAILURE (lift_status from spasm_lift, optional)
+ * and fills result; best_values (B,T,dof) receives the accepted trajectory. The per-outer
+ * records (OuterRecord) stay in the workspace: spasm_al_records gives their device
+ * pointers {mu, lam, cons, upd, obj, viol, feas, first_feasible, n_outers, best_x}, each
+ * [outer][P] (x3 for lam/cons/upd). */
+int64_t spasm_al_workspace_bytes(const spasm_traj* traj, int dtype, int64_t P, const spasm_al_config* cfg);
+int spasm_al_records(const spasm_traj* traj, int dtype, int64_t P, const spasm_al_config* cfg, void* workspace,
+                     void* ptrs[10]);
+int spasm_solve_al(const spasm_traj* traj, int dtype, const spasm_al_config* cfg, const void* values, int64_t P,
+                   const int32_t* n_active, const int32_t* lift_status, void* workspace, int64_t workspace_bytes,
+                   void* best_values, spasm_al_result* result, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -65,6 +65,75 @@ class spasm_solve_report(ctypes.Structure):
     ]
 
 
+class spasm_chain(ctypes.Structure):
+    _fields_ = [
+        ("dof", c_int32),
+        ("n_spheres", c_int32),
+        ("axes", c_void_p),
+        ("offsets", c_void_p),
+        ("lower", c_void_p),
+        ("upper", c_void_p),
+        ("tool_translation", c_void_p),
+        ("tool_rotation", c_void_p),
+        ("sphere_centers", c_void_p),
+        ("sphere_radii", c_void_p),
+        ("sphere_link", c_void_p),
+    ]
+
+
+class spasm_traj_desc(ctypes.Structure):
+    _fields_ = [
+        ("manipulation", c_int32),
+        ("n_blocks", c_int32),
+        ("spheres_per_block", c_void_p),
+        ("block_centers", c_void_p),
+        ("block_radii", c_void_p),
+        ("staged_poses", c_void_p),
+        ("grasp_offset", c_void_p),
+        ("grasp_yaw_offset", c_double),
+        ("n_static", c_int32),
+        ("static_centers", c_void_p),
+        ("static_radii", c_void_p),
+        ("place_model", c_void_p),
+        ("anchor_yaw", c_int32),
+        ("rows_have_yaw", c_int32),
+        ("start", c_void_p),
+        ("goal", c_void_p),
+    ]
+
+
+class spasm_al_config(ctypes.Structure):
+    _fields_ = [
+        ("w_start", c_double),
+        ("w_arm", c_double),
+        ("w_block", c_double),
+        ("w_place", c_double),
+        ("mu0", c_double),
+        ("beta", c_double),
+        ("lr_init", c_double),
+        ("lr_final", c_double),
+        ("validation_epsilon", c_double),
+        ("outer_iters", c_int32),
+        ("inner_steps", c_int32),
+        ("place_mode", c_int32),
+        ("waypoints", c_int32),
+    ]
+
+
+class spasm_al_result(ctypes.Structure):
+    _fields_ = [
+        ("status", c_int32),
+        ("accepted_outer", c_int32),
+        ("particle_index", c_int32),
+        ("n_outers", c_int32),
+        ("n_particles", c_int32),
+        ("lift_pick_fail", c_int32),
+        ("objective", c_double),
+        ("least_violation", c_double),
+        ("device_ms", c_double),
+    ]
+
+
 # name -> (restype, argtypes); the full exported surface of include/spasm.h
 SIGNATURES = {
     "spasm_last_error": (c_char_p, []),
@@ -111,6 +180,42 @@ SIGNATURES = {
         c_int,
         [c_void_p, c_int, POINTER(spasm_solve_config), c_void_p, c_int64, c_void_p, c_int64, c_void_p, c_void_p,
          c_void_p, POINTER(spasm_solve_report), c_void_p, c_void_p, c_void_p, c_void_p],
+    ),
+    "spasm_traj_create": (c_int, [POINTER(c_void_p), POINTER(spasm_chain), POINTER(spasm_traj_desc)]),
+    "spasm_traj_destroy": (None, [c_void_p]),
+    "spasm_traj_segments": (c_int, [c_void_p]),
+    "spasm_fk": (c_int, [c_void_p, c_int, c_void_p, c_int64, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
+                         c_void_p]),
+    "spasm_ik_solve": (
+        c_int,
+        [c_void_p, c_int, c_void_p, c_void_p, c_int64, c_uint64, c_int, c_int, c_double, c_void_p, c_void_p,
+         c_void_p, c_void_p],
+    ),
+    "spasm_polish_tool_down": (c_int, [c_void_p, c_int, c_void_p, c_void_p, c_void_p, c_int64, c_void_p, c_void_p]),
+    "spasm_traj_evaluate": (
+        c_int,
+        [c_void_p, c_int, POINTER(spasm_al_config), c_void_p, c_int64, c_int, c_int, c_void_p, c_void_p, c_int,
+         c_void_p, c_void_p, c_void_p, c_void_p, c_void_p],
+    ),
+    "spasm_traj_validate": (
+        c_int, [c_void_p, c_int, POINTER(spasm_al_config), c_void_p, c_int64, c_void_p, c_void_p, c_void_p]),
+    "spasm_lift_workspace_bytes": (c_int64, [c_void_p, c_int, c_int64, c_int]),
+    "spasm_lift": (
+        c_int,
+        [c_void_p, c_int, c_void_p, c_int64, c_int, c_uint64, c_int, c_void_p, c_int64, c_void_p, c_void_p,
+         c_void_p, c_void_p],
+    ),
+    "spasm_trajectory_stream_state": (c_int, [c_uint64, POINTER(c_uint64)]),
+    "spasm_init_trajectories": (
+        c_int,
+        [c_void_p, c_int, c_void_p, c_int64, c_int, c_void_p, c_int, c_int, POINTER(c_uint64), c_void_p, c_void_p],
+    ),
+    "spasm_al_workspace_bytes": (c_int64, [c_void_p, c_int, c_int64, POINTER(spasm_al_config)]),
+    "spasm_al_records": (c_int, [c_void_p, c_int, c_int64, POINTER(spasm_al_config), c_void_p, POINTER(c_void_p)]),
+    "spasm_solve_al": (
+        c_int,
+        [c_void_p, c_int, POINTER(spasm_al_config), c_void_p, c_int64, c_void_p, c_void_p, c_void_p, c_int64,
+         c_void_p, POINTER(spasm_al_result), c_void_p],
     ),
 }
 

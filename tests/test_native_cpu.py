@@ -75,3 +75,41 @@ def test_no_cpu_fallback_without_gpu():
     m = as_cost_model(load_scene("tetris5").problem)
     with pytest.raises(nat.NativeError):
         m.evaluate(np.zeros((2, 15)), "linear")
+
+
+def test_traj_handles_build_without_gpu():
+    """spasm_traj_create is host-only (device tables upload lazily): every robot scene's
+    _Geometry builds here, and malformed descriptions are rejected with SPASM_ERR_USAGE."""
+    from paper_2510_07674_b200 import trajopt as tj
+    from paper_2510_07674_b200.problems import load_scene
+
+    for name in ("tower4", "tetris5", "single1", "tower3c", "corridor3"):
+        sc = load_scene(name)
+        geo = tj._geometry(sc.problem, sc.chain, sc.grasp, None, None)
+        assert nat.load().spasm_traj_segments(geo.handle) == geo.n_segments
+    lib = nat.load()
+    ch = nat.spasm_chain()
+    ch.dof = 9  # > 8 joints
+    d = nat.spasm_traj_desc()
+    h = ctypes.c_void_p()
+    assert lib.spasm_traj_create(ctypes.byref(h), ctypes.byref(ch), ctypes.byref(d)) == nat.SPASM_ERR_USAGE
+    assert "dof" in nat.last_error()
+
+
+def test_trajectory_stream_state_matches_numpy():
+    for seed in (0, 1, 77, 2**33 + 5):
+        out = (ctypes.c_uint64 * 4)()
+        assert nat.load().spasm_trajectory_stream_state(seed, out) == 0
+        st = np.random.PCG64(np.random.SeedSequence(entropy=seed, spawn_key=(1 << 20,))).state["state"]
+        assert (out[0] << 64) | out[1] == st["state"]
+        assert (out[2] << 64) | out[3] == st["inc"]
+
+
+def test_trajopt_config_validation_mirrors_reference():
+    from paper_2510_07674_b200.trajopt import TrajOptConfig
+
+    assert TrajOptConfig(k_waypoint=1, k_interp=5).waypoints_per_segment == 11
+    for bad in ({"k_waypoint": -1}, {"k_interp": 0}, {"w_start": -1.0}, {"mu0": 0.0}, {"beta": 1.0},
+                {"outer_iters": 0}, {"inner_steps": 0}, {"lr_init": 0.0}, {"validation_epsilon": 0.0}):
+        with pytest.raises(ValueError):
+            TrajOptConfig(**bad)
