@@ -23,6 +23,16 @@
 #include "seedseq.cuh"
 #include "stage2_launch.cuh"
 
+// launchers are instantiated in stage2_f32.cu / stage2_f64.cu only
+#define SPASM_TEMPLATE_PREFIX extern
+#define SPASM_R float
+#include "stage2_inst.inc"
+#undef SPASM_R
+#define SPASM_R double
+#include "stage2_inst.inc"
+#undef SPASM_R
+#undef SPASM_TEMPLATE_PREFIX
+
 struct spasm_model : public spasm::Model {};
 struct spasm_traj : public spasm::Traj {};
 
