@@ -1,14 +1,18 @@
 """Benchmark: SPaSM two-stage particle optimizer on B200 (BASELINE.json metric).
 
-One "step" = one full stage-1 solve (sample -> stable top-M -> fused K_lin+K_quad descent
--> satisfying extraction + re-check, restarts included) of the workload's scene on
-synthetic, on-device-sampled particles, through the reference-facing API
-``particle_opt.solve`` (host config in, host placements out).
+One "step" is one full ``solve_scene`` call (reference bench.py:168-268) through the
+public API: host scene + config in, host placement + trajectory out. It runs stage 1
+(sample, stable top-M, fused K_lin+K_quad descent, satisfying extraction, restarts) and,
+when the workload's scene carries a robot, stage 2 (grasp IK lifting, trajectory init,
+and the persistent augmented-Lagrangian solve). The default workload is BASELINE
+configs[1] (C2: 3-block stacking with cuboid obstacles, 16k particles, full pipeline).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c2|c3|c5] [--impl b200|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c1|c2|c3|c5]
+                    [--precision fp32|fp64] [--impl b200|reference]
 
 Multi-GPU (torchrun, one rank per GPU): each rank solves its own seeds (replicas, weak
-scaling); rank 0 prints one JSON line with whole-job throughput over max-over-ranks time.
+scaling, no data-path collective); rank 0 prints one JSON line with whole-job throughput
+over the max-over-ranks time.
 """
 from __future__ import annotations
 
@@ -16,7 +20,6 @@ import argparse
 import json
 import os
 import statistics
-import subprocess
 import sys
 import threading
 import time
@@ -28,107 +31,139 @@ sys.path.insert(0, ROOT)
 
 METRIC = "solve time ms (p50) at 100% success; particle-iterations/sec at 1/2/4/8 B200"
 
+# name: (scene, solver overrides, stage-1 only, description)
 WORKLOADS = {
-    # name: (scene, overrides, description)
-    "c2": ("tower3c", {"n": 16384, "m": 2048},
-           "C2 3-block stacking with cuboid obstacles (sphere-grid cuboids), 16k particles, stage 1"),
-    "c3": ("tetris5", {"n": 65536, "m": 8192},
-           "C3 Tetris packing, 5 objects, 64k particles, stage 1"),
-    "c5": ("tetris8", {"n": 1 << 20, "m": 1 << 17},
-           "C5 8-object skeleton, 1M particles (M = N/8), stage 1"),
+    "c1": ("single1", {}, False,
+           "C1 7-DOF arm, single-block pick-and-place, 1024 particles, stage 1 + stage 2 (32 waypoints)"),
+    "c2": ("tower3c", {}, False,
+           "C2 3-block stacking with cuboid obstacles (sphere-grid cuboids), 16k particles, stage 1 + stage 2"),
+    "c3": ("tetris5", {"n": 65536, "m": 8192}, True, "C3 Tetris packing, 5 objects, 64k particles, stage 1"),
+    "c5": ("tetris8", {"n": 1 << 20, "m": 1 << 17}, True, "C5 8-object skeleton, 1M particles (M = N/8), stage 1"),
 }
 
 
-def flops_per_particle_iteration(model, mode="linear"):
-    """Algorithmic FP32 FLOPs of one fused cost-gradient-update step."""
+# ---------------------------------------------------------------------------
+# algorithmic work counts
+# ---------------------------------------------------------------------------
+def stage1_flops_per_iteration(model, mode="linear"):
+    """FP32 FLOPs of one fused cost-gradient-update step of one particle."""
     from paper_2510_07674_b200.problems import TetrisCostModel
 
     p = model.problem
     D = model.dimension
     if isinstance(model, TetrisCostModel):
         n = p.n_blocks
-        S = sum(len(b.sphere_set) for b in p.blocks)
         counts = [len(b.sphere_set) for b in p.blocks]
+        S = sum(counts)
         E = sum(counts[i] * counts[j] for i in range(n) for j in range(i + 1, n)) + S * len(p.wall_radii)
-        per_pair = 22 if mode == "linear" else 24
-        f = per_pair * E + 3 * S + 4 * n + 2 * D
+        f = (22 if mode == "linear" else 24) * E + 3 * S + 4 * n + 2 * D
         if model.free_yaw:
             f += 10 * E + 8 * S
         return f
     B = p.n_blocks
     O = len(p.obstacle_radii)
-    pairs = B * (B - 1) // 2
-    return 22 * (pairs + B * O) + 30 * (B - 1) + 4 * B + 2 * D
+    return 22 * (B * (B - 1) // 2 + B * O) + 30 * (B - 1) + 4 * B + 2 * D
 
 
+def al_flops_per_inner_step(scene, T):
+    """FLOPs of one AL inner step (value + exact gradient + clamped update) of one trajectory
+    particle, counted from the shapes (trajopt.py:416-653, 993-1002):
+      FK per waypoint 124 per joint + 18 per arm sphere + 63 (tool frame);
+      path length 4 per dof + 1; sphere-pair penetration + gradient 20 per pair;
+      held-block sphere placement 18; Jacobian-transpose products 15 per sphere + 17 per
+      joint (arm) and per joint again (held); start/placement chains 40 per joint per
+      segment; update 4 per dof."""
+    chain = scene.chain
+    J = chain.dof
+    S = len(chain.sphere_table()[1])
+    prob = scene.problem
+    n_static = len(scene.obstacle_radii)
+    if hasattr(prob, "blocks") or hasattr(prob, "n_blocks"):
+        counts = [1] * prob.n_blocks if not hasattr(prob, "blocks") else [len(b.sphere_set) for b in prob.blocks]
+    else:
+        counts = []
+    B = max(1, len(counts))
+    f = 0
+    for b in range(B):
+        later = sum(counts[b + 1:]) if counts else 0
+        earlier = sum(counts[:b]) if counts else 0
+        obs = n_static + later + earlier
+        SB = counts[b] if counts else 0
+        for t in range(T):
+            f += 124 * J + 18 * S + 63 + 4 * J + 1 + 20 * S * obs + 15 * S + 17 * J + 4 * J
+            if counts and 1 <= t <= T - 2:
+                f += 18 * SB + 20 * SB * obs + 15 * SB + 17 * J
+        f += 40 * J
+    return f
+
+
+# ---------------------------------------------------------------------------
+# clocks during the timed region (NVML polled every 2 ms)
+# ---------------------------------------------------------------------------
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
+    REASONS = {"hw_slowdown": "nvmlClocksEventReasonHwSlowdown",
+               "hw_thermal_slowdown": "nvmlClocksEventReasonHwThermalSlowdown",
+               "sw_thermal_slowdown": "nvmlClocksEventReasonSwThermalSlowdown",
+               "sw_power_cap": "nvmlClocksEventReasonSwPowerCap",
+               "hw_power_brake": "nvmlClocksEventReasonHwPowerBrakeSlowdown"}
 
-    def __init__(self, index=0):
+    def __init__(self, index=0, period=0.002):
         self.index = index
-        self.rows = []
-        self.proc = None
+        self.period = period
+        self.sm = []
+        self.bits = 0
+        self.max_mhz = None
+        self._stop = threading.Event()
+        self._ok = False
 
     def __enter__(self):
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.index), "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
-                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
-                 "--format=csv,noheader,nounits", "-lms", "50"],
-                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.thread = threading.Thread(target=self._read, daemon=True)
-            self.thread.start()
-        except FileNotFoundError:
-            self.proc = None
+            import pynvml
+
+            pynvml.nvmlInit()
+            self._nv = pynvml
+            self._h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM)
+            self._ok = True
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+        except Exception:  # no NVML: report no samples
+            self._ok = False
         return self
 
-    def _read(self):
-        for line in self.proc.stdout:
-            self.rows.append([x.strip() for x in line.split(",")])
+    def _run(self):
+        nv = self._nv
+        while not self._stop.is_set():
+            try:
+                self.sm.append(nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM))
+                self.bits |= nv.nvmlDeviceGetCurrentClocksEventReasons(self._h)
+            except Exception:
+                pass
+            time.sleep(self.period)
 
     def __exit__(self, *exc):
-        if self.proc is not None:
-            self.proc.terminate()
-            try:
-                self.proc.wait(timeout=2)
-            except subprocess.TimeoutExpired:
-                self.proc.kill()
+        self._stop.set()
+        if self._ok:
+            self._t.join(timeout=1)
 
     def summary(self):
-        sm = [float(r[0]) for r in self.rows if len(r) >= 7 and r[0].replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in self.rows if len(r) >= 7 and r[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i - 3] for r in self.rows if len(r) >= 7 for i in range(3, 7)
-                          if r[i].lower() == "active"})
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(sm)}
+        reasons = []
+        if self._ok:
+            for name, attr in self.REASONS.items():
+                if self.bits & int(getattr(self._nv, attr, 0)):
+                    reasons.append(name)
+        return {"sm_mhz": statistics.median(self.sm) if self.sm else None, "sm_max_mhz": self.max_mhz,
+                "reasons": reasons, "samples": len(self.sm), "source": "nvml (2 ms polling during the timed region)"}
 
 
 def dist_env():
-    rank = int(os.environ.get("RANK", "0"))
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    return rank, world, local
-
-
-def build_workload(name, precision):
-    from paper_2510_07674_b200 import particle_opt as po
-    from paper_2510_07674_b200.bench_api import effective_max_restarts
-    from paper_2510_07674_b200.problems import as_cost_model, load_scene
-
-    scene_name, over, desc = WORKLOADS[name]
-    scene = load_scene(scene_name)
-    model = as_cost_model(scene.problem, precision=precision)
-    base = {**scene.solver_overrides, **over}
-    cfg = po.OptimizerConfig(**base)
-    cfg.max_restarts = effective_max_restarts(cfg)
-    return scene, model, cfg, desc
+    return int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("LOCAL_RANK",
+                                                                                                          "0"))
 
 
 def measure_schedule_kernel(model, cfg, repeats=10):
-    """Average device time of the fused descent kernel (dominant kernel) on one M-row batch,
-    timed with CUDA events on the launching stream."""
+    """Average device time of the fused stage-1 descent kernel on one M-row batch (CUDA
+    events on the launching stream, L2 flushed between launches)."""
     import torch
 
     from paper_2510_07674_b200 import _native as nat
@@ -161,10 +196,16 @@ def measure_schedule_kernel(model, cfg, repeats=10):
         e1.synchronize()
         times.append(e0.elapsed_time(e1))
     ms = statistics.mean(times)
-    f_lin = flops_per_particle_iteration(model, "linear")
-    f_quad = flops_per_particle_iteration(model, "quadratic")
-    flops = cfg.m * (cfg.k_lin * f_lin + cfg.k_quad * f_quad)
+    flops = cfg.m * (cfg.k_lin * stage1_flops_per_iteration(model, "linear")
+                     + cfg.k_quad * stage1_flops_per_iteration(model, "quadratic"))
     return ms, flops
+
+
+def _traffic(key):
+    path = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(path):
+        return json.load(open(path)).get(key)
+    return None
 
 
 def run_b200(args):
@@ -178,159 +219,184 @@ def run_b200(args):
         dist.init_process_group("nccl")
     else:
         torch.cuda.set_device(0)
-    from paper_2510_07674_b200 import particle_opt as po
+    from paper_2510_07674_b200.bench_api import _solver_config, effective_max_restarts, solve_scene
+    from paper_2510_07674_b200.problems import as_cost_model, load_scene
 
-    scene, model, cfg, desc = build_workload(args.workload, args.precision)
+    scene_name, over, stage1_only, desc = WORKLOADS[args.workload]
+    scene = load_scene(scene_name)
+    model = as_cost_model(scene.problem, precision=args.precision)
+    cfg = _solver_config(scene, 0, over, False)
+    cfg.max_restarts = effective_max_restarts(cfg)
+
+    def step(seed):
+        return solve_scene(scene, seed=seed, solver_overrides=over, no_trajopt=stage1_only, precision=args.precision,
+                           model=model)
+
     seed0 = 1000 * rank
-    # warm-up (also builds workspaces / loads modules)
     for i in range(args.warmup):
-        cfg.seed = seed0 + 100000 + i
-        po.solve(model, cfg)
+        step(seed0 + 100000 + i)
     torch.cuda.synchronize()
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")  # > 126 MB L2
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
     stream = torch.cuda.current_stream()
-    dev_ms, wall_ms, pits, evals, succ, launches = [], [], 0, 0, 0, 0
+    dev_ms, wall_ms, sols = [], [], []
     with ClockSampler(local) as clocks:
         for i in range(args.steps):
-            flush.fill_(i & 0xFF)  # L2 flush between timed iterations (outside the events)
-            cfg.seed = seed0 + i
+            flush.fill_(i & 0xFF)  # L2 flush between timed solves (outside the events)
+            torch.cuda.synchronize()
             e0 = torch.cuda.Event(enable_timing=True)
             e1 = torch.cuda.Event(enable_timing=True)
-            torch.cuda.synchronize()
             t0 = time.perf_counter()
             e0.record(stream)
-            res = po.solve(model, cfg)  # host config in, host placements out (e2e path)
+            sol = step(seed0 + i)
             e1.record(stream)
             e1.synchronize()
             wall_ms.append((time.perf_counter() - t0) * 1e3)
             dev_ms.append(e0.elapsed_time(e1))
-            restarts_run = min(res.report.restarts + 1, cfg.max_restarts) if res.success else cfg.max_restarts
-            pits += restarts_run * cfg.m * (cfg.k_lin + cfg.k_quad)
-            evals += restarts_run * cfg.n
-            succ += int(res.success)
-            launches += res.report.launches
-    total_dev = sum(dev_ms)
-    total_wall = sum(wall_ms)
+            sols.append(sol)
+    its = sum(s.stats.get("stage1_iterations", 0) + s.stats.get("stage2_iterations", 0) for s in sols)
+    succ = sum(int(s.success) for s in sols)
+    launches = sum(s.stats.get("stage1_launches", 0) + s.stats.get("stage2_launches", 0) for s in sols)
+    al_ms = [s.stats["al_device_ms"] for s in sols if "al_device_ms" in s.stats]
+    al_its = sum(s.stats.get("stage2_iterations", 0) for s in sols)
+    total_dev, total_wall = sum(dev_ms), sum(wall_ms)
     if world > 1:
         t = torch.tensor([total_dev, total_wall], device="cuda", dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total_dev, total_wall = t.tolist()
-        c = torch.tensor([pits, succ, launches], device="cuda", dtype=torch.float64)
+        c = torch.tensor([its, succ, launches], device="cuda", dtype=torch.float64)
         dist.all_reduce(c)
-        pits, succ, launches = [int(v) for v in c.tolist()]
-    kern_ms, kern_flops = measure_schedule_kernel(model, cfg)
+        its, succ, launches = [int(v) for v in c.tolist()]
     clk = clocks.summary()
+    sm_mhz = clk["sm_mhz"] or 1965.0
+    peak = 2 * 128 * 148 * sm_mhz * 1e6 / 1e12  # FP32 CUDA-core TFLOP/s at the measured SM clock
+    if not stage1_only and al_ms:
+        T = load_scene(scene_name).trajopt_overrides.get("k_interp", 5) * (
+            load_scene(scene_name).trajopt_overrides.get("k_waypoint", 1) + 1) + 1
+        f_step = al_flops_per_inner_step(scene, T)
+        kern_ms = statistics.mean(al_ms)
+        flops = f_step * al_its / len(al_ms)
+        roof = {"bound": "fp32", "achieved": flops / (kern_ms * 1e-3) / 1e12, "peak": peak, "unit": "TFLOP/s",
+                "kernel": "k_solve_al (persistent AL solve, CTA per trajectory particle)", "kernel_ms": kern_ms,
+                "flops_per_launch": flops, "flops_per_inner_step": f_step,
+                "traffic": _traffic(f"{args.workload}_{args.precision}_k_solve_al"),
+                "note": "latency-bound: a few dozen CTAs x serial inner steps; see DESIGN.md section 3"}
+    else:
+        kern_ms, flops = measure_schedule_kernel(model, cfg)
+        roof = {"bound": "fp32", "achieved": flops / (kern_ms * 1e-3) / 1e12, "peak": peak, "unit": "TFLOP/s",
+                "kernel": "k_schedule (fused K_lin+K_quad descent)", "kernel_ms": kern_ms, "flops_per_launch": flops,
+                "traffic": _traffic(f"{args.workload}_{args.precision}_k_schedule")}
+    roof["frac"] = roof["achieved"] / peak
+    roof["peak_note"] = ("FP32 CUDA-core 2*128*148*f_SM at the median SM clock sampled under load "
+                         "(MEASURED_PEAKS.json has no FP32 figure)")
     if rank != 0:
         if world > 1:
             dist.destroy_process_group()
         return
-    sm_mhz = clk["sm_mhz"] or 1965.0
-    peak = 2 * 128 * 148 * sm_mhz * 1e6 / 1e12  # FP32 CUDA-core TFLOP/s at the measured SM clock
-    achieved = kern_flops / (kern_ms * 1e-3) / 1e12
-    traffic = None
-    tpath = os.path.join(ROOT, "profiles", "traffic.json")
-    if os.path.exists(tpath):
-        traffic = json.load(open(tpath)).get(f"{args.workload}_{args.precision}")
-    cpu = cpu_baseline(args) if (rank == 0 and world == 1 and not args.no_cpu) else None
+    cpu = cpu_baseline(args) if (world == 1 and not args.no_cpu) else None
+    D = model.dimension
+    p_ret = cfg.p_return
+    h2d = 0 if stage1_only else p_ret * D * 8  # stage-1 placements re-enter the device for lifting
+    d2h = 64 + p_ret * (D + 3) * 8
+    if not stage1_only:
+        t_wp = sols[0].trajectory.segments.size if sols and sols[0].trajectory is not None else 0
+        d2h += 64 + 8 * t_wp
     line = {
         "metric": METRIC,
-        "value": pits / (total_dev * 1e-3),
+        "value": its / (total_dev * 1e-3),
         "unit": "particle-iterations/s",
         "n_gpus": world,
         "steps": args.steps,
         "warmup": args.warmup,
         "ms_per_step": total_dev / args.steps,
-        "p50_solve_ms": statistics.median(dev_ms),
+        "p50_solve_ms": statistics.median(wall_ms),
         "success_rate": succ / (args.steps * world),
         "higher_is_better": True,
         "scaling": "weak",
         "vs_baseline": None,
         "dtype": "f32" if args.precision == "fp32" else "f64",
-        "data": "synthetic (scene tables; particles sampled on device from numpy-identical PCG64 restart streams)",
-        "config": {"workload": desc, "scene": WORKLOADS[args.workload][0], "n": cfg.n, "m": cfg.m,
-                   "k_lin": cfg.k_lin, "k_quad": cfg.k_quad, "max_restarts": cfg.max_restarts,
-                   "l2": "flushed (256 MB write) between timed solves", "parallelism": f"replicas x{world}"},
-        "e2e": {"value": pits / (total_wall * 1e-3), "unit": "particle-iterations/s",
-                "p50_solve_ms": statistics.median(wall_ms),
-                "h2d_bytes_per_step": 0, "d2h_bytes_per_step": int(64 + cfg.p_return * (model.dimension + 3) * 8)},
-        "roofline": {"bound": "fp32", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                     "frac": achieved / peak, "traffic": traffic, "kernel": "k_schedule (fused descent)",
-                     "kernel_ms": kern_ms, "flops_per_launch": kern_flops,
-                     "peak_note": "FP32 CUDA-core 2*128*148*f_SM at the median SM clock sampled under load "
-                                  "(no FP32 figure in MEASURED_PEAKS.json)"},
+        "data": "synthetic (bundled scene tables; particles drawn on device from numpy-identical PCG64 streams)",
+        "config": {"workload": desc, "scene": scene_name, "n": cfg.n, "m": cfg.m, "k_lin": cfg.k_lin,
+                   "k_quad": cfg.k_quad, "max_restarts": cfg.max_restarts, "p_return": p_ret,
+                   "stage2": not stage1_only, "l2": "flushed (256 MB write) between timed solves",
+                   "parallelism": f"replicas x{world}"},
+        "e2e": {"value": its / (total_wall * 1e-3), "unit": "particle-iterations/s",
+                "p50_solve_ms": statistics.median(wall_ms), "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                "api": "bench_api.solve_scene (host scene/config in, host placement/trajectory out)"},
+        "roofline": roof,
         "cpu_baseline": cpu,
         "clocks": clk,
         "gpu_launches": launches,
-        "initial_evals_per_s": evals / (total_dev * 1e-3),
+        "breakdown": {"stage1_ms_mean": statistics.mean(s.stats.get("stage1_ms", 0.0) for s in sols),
+                      "al_device_ms_mean": statistics.mean(al_ms) if al_ms else None,
+                      "stage2_outers_mean": statistics.mean(s.stats.get("stage2_outers", 0) for s in sols)},
     }
     print(json.dumps(line))
     if world > 1:
         dist.destroy_process_group()
 
 
-def cpu_baseline(args, budget_s=15.0):
-    """The oracle port timed on this host's cores on a bounded sample of the workload."""
-    from oracle import stage1 as orc
+def _oracle_solve(scene, over, stage1_only, seed, threads, max_restarts=None):
+    from oracle import pipeline as op
+
+    return op.solve_scene(scene, seed=seed, threads=threads, solver_overrides=over, no_trajopt=stage1_only,
+                          max_restarts=max_restarts)
+
+
+def cpu_baseline(args, budget_s=20.0):
+    """The CPU oracle port (oracle/pipeline.py, float64 numpy) timed on this host's cores
+    on a bounded sample of the same workload."""
     from paper_2510_07674_b200.problems import load_scene
 
-    scene_name, over, desc = WORKLOADS[args.workload]
+    scene_name, over, stage1_only, desc = WORKLOADS[args.workload]
     scene = load_scene(scene_name)
-    o = orc.oracle_model(scene.problem)
-    base = {**scene.solver_overrides, **over}
     threads = os.cpu_count() or 1
-    cfg = orc.OracleConfig(**base)
-    pits, t_total, solves = 0, 0.0, 0
+    its, t_total, solves, times = 0, 0.0, 0, []
     t_start = time.perf_counter()
-    # bounded sample: one restart per solve (max_restarts=1), as many solves as fit the budget
+    # large stage-1-only workloads: one restart per sample solve; pipelines: whole solves
+    mr = 1 if stage1_only else None
     while time.perf_counter() - t_start < budget_s and solves < 3:
-        cfg.seed = solves
-        cfg.max_restarts = 1
-        t0 = time.perf_counter()
-        orc.solve(o, cfg, threads=threads)
-        t_total += time.perf_counter() - t0
-        pits += cfg.m * (cfg.k_lin + cfg.k_quad)
+        r = _oracle_solve(scene, over, stage1_only, solves, threads, max_restarts=mr)
+        t_total += r.time_ms * 1e-3
+        times.append(r.time_ms)
+        its += r.stage1_iterations + r.stage2_iterations
         solves += 1
-    return {"value": pits / t_total, "unit": "particle-iterations/s", "cores": threads, "kind": "port",
-            "sample": f"{solves} single-restart solve(s) of {scene_name} at n={cfg.n}, m={cfg.m} "
-                      f"(oracle/stage1.py, numpy float64, {threads} threads)"}
+    return {"value": its / t_total, "unit": "particle-iterations/s", "cores": threads, "kind": "port",
+            "p50_solve_ms": statistics.median(times),
+            "sample": f"{solves} {'single-restart stage-1' if stage1_only else 'full two-stage'} solve(s) of "
+                      f"{scene_name} (oracle/pipeline.py, numpy float64, {threads} threads)"}
 
 
 def run_reference(args):
     rank, world, _ = dist_env()
     if rank != 0:
         return
-    from oracle import stage1 as orc
     from paper_2510_07674_b200.problems import load_scene
 
-    scene_name, over, desc = WORKLOADS[args.workload]
+    scene_name, over, stage1_only, desc = WORKLOADS[args.workload]
     scene = load_scene(scene_name)
-    o = orc.oracle_model(scene.problem)
     threads = os.cpu_count() or 1
-    cfg = orc.OracleConfig(**{**scene.solver_overrides, **over})
-    cfg.max_restarts = 1  # bounded sample per step: one restart
-    for i in range(args.warmup):
-        cfg.seed = 100000 + i
-        if i == 0:
-            orc.solve(o, cfg, threads=threads)
-    times, pits = [], 0
+    mr = 1 if stage1_only else None
+    for i in range(args.warmup):  # warm numpy / thread pools on cheap stage-1 samples
+        _oracle_solve(scene, over, True, 100000 + i, threads, max_restarts=1)
+    times, its, succ = [], 0, 0
     for i in range(args.steps):
-        cfg.seed = i
-        t0 = time.perf_counter()
-        orc.solve(o, cfg, threads=threads)
-        times.append((time.perf_counter() - t0) * 1e3)
-        pits += cfg.m * (cfg.k_lin + cfg.k_quad)
-    value = pits / (sum(times) * 1e-3)
+        r = _oracle_solve(scene, over, stage1_only, i, threads, max_restarts=mr)
+        times.append(r.time_ms)
+        its += r.stage1_iterations + r.stage2_iterations
+        succ += int(r.success)
+    value = its / (sum(times) * 1e-3)
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "particle-iterations/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": sum(times) / args.steps,
-        "p50_solve_ms": statistics.median(times), "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": "f64", "data": "synthetic", "config": {"workload": desc, "scene": scene_name, "n": cfg.n,
-                                                        "m": cfg.m, "max_restarts": 1},
+        "p50_solve_ms": statistics.median(times), "success_rate": succ / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": desc, "scene": scene_name, **over, "stage2": not stage1_only,
+                   "max_restarts": mr if mr else "STEP_CAP"},
         "cpu_baseline": {"value": value, "unit": "particle-iterations/s", "cores": threads, "kind": "port",
-                         "sample": f"{args.steps} single-restart solves of {scene_name} (oracle/stage1.py)"},
+                         "sample": f"{args.steps} solves of {scene_name} (oracle/pipeline.py, numpy float64)"},
         "e2e": {"value": value, "unit": "particle-iterations/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line))
@@ -346,8 +412,7 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     args = ap.parse_args()
-    if args.warmup < 3:
-        args.warmup = 3
+    args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
         run_reference(args)
     else:

@@ -9,7 +9,7 @@ from __future__ import annotations
 
 import math
 import time
-from dataclasses import dataclass, replace
+from dataclasses import dataclass, field, replace
 from typing import Optional
 
 import numpy as np
@@ -49,6 +49,8 @@ class SceneSolution:
     trajectory: object = None
     path_length: Optional[float] = None
     max_violation: Optional[float] = None
+    # B200 extras (not in the reference): work and launch counts for the bench line
+    stats: dict = field(default_factory=dict)
 
 
 def solve_scene(scene: Scene, *, seed: int = 0, threads: int = 1, solver_overrides: Optional[dict] = None,
@@ -67,15 +69,21 @@ def solve_scene(scene: Scene, *, seed: int = 0, threads: int = 1, solver_overrid
     run_stage2 = scene.chain is not None and not no_trajopt
     t0 = time.perf_counter()
     result = solve(model, config, warm_seeds=warm_seeds, threads=threads)
+    restarts_run = result.report.restarts + 1 if result.success else config.max_restarts
+    stats = {"stage1_iterations": restarts_run * config.m * (config.k_lin + config.k_quad),
+             "stage1_evaluations": restarts_run * config.n, "stage1_launches": result.report.launches,
+             "stage1_ms": (time.perf_counter() - t0) * 1e3}
     if not result.success:
         return SceneSolution(False, (time.perf_counter() - t0) * 1e3, result.report.restarts, result.report.steps,
-                             math.nan)
+                             math.nan, stats=stats)
     if not run_stage2:
         time_ms = (time.perf_counter() - t0) * 1e3
         best = result.particles[0]
         ok = bool(np.asarray(model.satisfaction(best[None, :], config.epsilon))[0])
         return SceneSolution(ok, time_ms, result.report.restarts, result.report.steps, float(result.costs[0]),
-                             placement=best.copy())
+                             placement=best.copy(), stats=stats)
     from .trajopt import solve_stage2
 
-    return solve_stage2(scene, result, config, seed, trajopt_overrides, t0, precision=precision)
+    sol = solve_stage2(scene, result, config, seed, trajopt_overrides, t0, precision=precision)
+    sol.stats = {**stats, **sol.stats}
+    return sol

@@ -769,11 +769,16 @@ def solve_stage2(scene, result, config, seed, trajopt_overrides, t0, precision: 
     status, res, best, report = _solve_al_device(geo, values, tcfg, None, precision, n_active=lift.status[1:],
                                                  lift_status=lift.status, want_report=False)
     time_ms = (time.perf_counter() - t0) * 1e3
+    stats = {"stage2_particles": int(res.n_particles), "stage2_outers": int(res.n_outers),
+             "stage2_iterations": int(res.n_particles) * int(res.n_outers) * int(tcfg.inner_steps),
+             "stage2_launches": 6, "al_device_ms": float(res.device_ms), "lift_targets": len(pl) * geo.n_segments
+             + geo.n_segments}
     if status == nat.SPASM_LIFT_FAILURE:
-        return SceneSolution(False, time_ms, result.report.restarts, result.report.steps, math.nan)
+        return SceneSolution(False, time_ms, result.report.restarts, result.report.steps, math.nan, stats=stats)
     if status == nat.SPASM_AL_FAILURE:
         w = float(res.least_violation)
-        return SceneSolution(False, time_ms, result.report.restarts, result.report.steps, w, max_violation=w)
+        return SceneSolution(False, time_ms, result.report.restarts, result.report.steps, w, max_violation=w,
+                             stats=stats)
     traj = _particle_trajectory(best.double().cpu().numpy(), geo)
     feasible, worst = validate(traj, scene.problem, scene.chain, grasp=scene.grasp,
                                static_centers=scene.obstacle_centers, static_radii=scene.obstacle_radii,
@@ -781,7 +786,7 @@ def solve_stage2(scene, result, config, seed, trajopt_overrides, t0, precision: 
     kept = lift.kept[:int(res.n_particles)].cpu().numpy()
     return SceneSolution(bool(feasible), time_ms, result.report.restarts, result.report.steps, worst,
                          placement=np.asarray(result.particles)[int(kept[res.particle_index])].copy(),
-                         trajectory=traj, path_length=trajectory_path_length(traj), max_violation=worst)
+                         trajectory=traj, path_length=trajectory_path_length(traj), max_violation=worst, stats=stats)
 
 
 def solve_motion_scene(scene, seed, trajopt_overrides, precision: str = "fp32"):
@@ -798,10 +803,13 @@ def solve_motion_scene(scene, seed, trajopt_overrides, precision: str = "fp32"):
     values = _init_async(geo, ends, None, tcfg, _pcg_state(trajectory_stream(seed)), precision)
     status, res, best, report = _solve_al_device(geo, values, tcfg, None, precision, want_report=False)
     time_ms = (time.perf_counter() - t0) * 1e3
+    stats = {"stage2_particles": 1, "stage2_outers": int(res.n_outers),
+             "stage2_iterations": int(res.n_outers) * int(tcfg.inner_steps), "stage2_launches": 4,
+             "al_device_ms": float(res.device_ms)}
     if status == nat.SPASM_AL_FAILURE:
         w = float(res.least_violation)
-        return SceneSolution(False, time_ms, 0, 0, w, max_violation=w)
+        return SceneSolution(False, time_ms, 0, 0, w, max_violation=w, stats=stats)
     traj = _particle_trajectory(best.double().cpu().numpy(), geo)
     feasible, worst = validate(traj, scene.problem, scene.chain, epsilon=tcfg.validation_epsilon, precision="fp64")
     return SceneSolution(bool(feasible), time_ms, 0, 0, worst, trajectory=traj,
-                         path_length=trajectory_path_length(traj), max_violation=worst)
+                         path_length=trajectory_path_length(traj), max_violation=worst, stats=stats)
