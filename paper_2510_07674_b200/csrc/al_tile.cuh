@@ -1,0 +1,885 @@
+// The augmented-Lagrangian engine of stage 2, one CTA per trajectory particle.
+//
+// Thread mapping: one 8-lane tile per waypoint w = (segment b, step t), lane j = joint j
+// (W = B*T tiles), plus one auxiliary warp for per-segment work. Per inner step:
+//
+//   P1 tiles: tile FK of the waypoint (coop.cuh), arm-sphere centres of link j on lane j,
+//             held-block spheres round-robin over lanes, path-length leg, start terms.
+//   P2 tiles: penetrations vs the segment's fixed obstacles (statics + later staged blocks).
+//      aux:   placed block poses from the final waypoints, then the free-yaw placement
+//             twin's cost + gradient (trajopt.py:448-472, 531-539), overlapping P2.
+//   P3 tiles: penetrations vs earlier placed blocks, their placed-pose partials (tile
+//             reduced), Jacobian-transpose products: lane k gets
+//             z_k . (sum_{link>=k} a x g - o_k x sum_{link>=k} g) from a suffix scan.
+//   P4       totals, constraint vector, multiplier scales; aux reduces placed partials.
+//   P5 tiles: lane k assembles dL/dq_k (path length, arm, held, placement chain through the
+//             final-waypoint Jacobian and exact yaw Jacobian, start alignment) and either
+//             stores it or applies the clamped descent step in place.
+//
+// Reductions run in a fixed order (xor trees, ordered loops; no atomics): deterministic.
+// Reference: trajopt.py:396-653 (value + gradient), 936-1063 (solve), 1071-1153 (validate).
+#pragma once
+#include "coop.cuh"
+#include "stage1_models.cuh"
+
+namespace spasm {
+
+// ---- placement twin (the free-yaw copy of the stage-1 model, trajopt.py:281-302) ------
+template <typename R>
+struct NoTwin {
+  int dim;
+};
+template <typename R, int KIND> struct TwinSceneOf { using type = NoTwin<R>; };
+template <typename R> struct TwinSceneOf<R, 1> { using type = TetrisScene<R>; };
+template <typename R> struct TwinSceneOf<R, 2> { using type = TowerScene<R>; };
+
+template <typename R, int KIND, int SPB, bool WG, bool Q>
+__device__ __forceinline__ R twin_run_t(const typename TwinSceneOf<R, KIND>::type& ts, const R* rows, R* grad,
+                                        R* scr) {
+  if constexpr (KIND == 1) {
+    return TetrisEval<R, SPB, true>::template run<true, WG, Q>(ts, rows, grad, scr, 1);
+  } else if constexpr (KIND == 2) {
+    return TowerEval<R, true>::template run<true, WG, Q>(ts, rows, grad, scr, 1);
+  } else {
+    return R(0);
+  }
+}
+
+template <typename R, int KIND, int SPB>
+__device__ __forceinline__ R twin_run(const typename TwinSceneOf<R, KIND>::type& ts, const R* rows, R* grad, R* scr,
+                                      bool want_grad, bool quad) {
+  if (want_grad) {
+    return quad ? twin_run_t<R, KIND, SPB, true, true>(ts, rows, grad, scr)
+                : twin_run_t<R, KIND, SPB, true, false>(ts, rows, grad, scr);
+  }
+  return quad ? twin_run_t<R, KIND, SPB, false, true>(ts, rows, grad, scr)
+              : twin_run_t<R, KIND, SPB, false, false>(ts, rows, grad, scr);
+}
+
+
+constexpr int kMaxAlThreads = 512;  // 60 waypoint tiles + the aux warp; <= 128 registers
+constexpr int kXS = 8;  // row stride of x / g / unit in shared memory ([w][joint])
+
+struct AlLayout {
+  int W, NW, nthreads, nwarps, J, B, T, S, SB, NB;
+  int scene, x, g, unit, ee, rot, armw, ga, hp, gh, pg, pl, seg, rows, gpose, scr, pgsum, red, scal, flags;
+  int total;
+};
+
+template <typename R>
+__host__ __device__ inline AlLayout al_layout(int B, int T, int J, int S, int SB, int NB) {
+  AlLayout L;
+  L.W = B * T;
+  L.NW = (L.W * kTile + 31) / 32 * 32;
+  L.nthreads = L.NW + 32;
+  L.nwarps = L.nthreads / 32;
+  L.J = J;
+  L.B = B;
+  L.T = T;
+  L.S = S;
+  L.SB = SB;
+  L.NB = NB;
+  const int W = L.W;
+  const int r = (int)sizeof(R);
+  int off = 0;
+  auto take = [&off](int bytes) {
+    const int o = off;
+    off += (bytes + 15) & ~15;
+    return o;
+  };
+  L.scene = take((int)sizeof(TrajScene<R>));
+  L.x = take(W * kXS * r);
+  L.g = take(W * kXS * r);
+  L.unit = take(W * kXS * r);
+  L.ee = take(3 * W * r);
+  L.rot = take(9 * W * r);
+  L.armw = take(3 * (S > 0 ? S : 1) * W * r);
+  L.ga = take(3 * (S > 0 ? S : 1) * W * r);
+  L.hp = take(3 * (SB > 0 ? SB : 1) * W * r);
+  L.gh = take(3 * (SB > 0 ? SB : 1) * W * r);
+  L.pg = take(8 * B * W * r);
+  L.pl = take(3 * (NB > 0 ? NB : 1) * r);
+  L.seg = take(3 * B * r);  // psi | cp | sp
+  L.rows = take(4 * B * r);
+  L.gpose = take(4 * B * r);
+  L.scr = take((2 * B + 2) * r);
+  L.pgsum = take(8 * B * r);
+  L.red = take(4 * L.nwarps * r);
+  L.scal = take(32 * r);
+  L.flags = take(16 * 4);
+  L.total = off;
+  return L;
+}
+
+// scal[] slots
+enum : int {
+  kObj = 0, kCarm, kCblk, kCplace, kLag, kCons0, kCons1, kCons2, kSc0, kSc1, kSc2, kLam0, kLam1, kLam2, kMu, kPrev,
+  kWorst, kLr
+};
+
+template <typename R>
+struct AlCtx {
+  AlLayout L;
+  TrajScene<R>* sc;
+  R *x, *g, *unit, *ee, *rot, *armw, *ga, *hp, *gh, *pg, *pl, *psi, *cp, *sp, *rows, *gpose, *scr, *pgsum, *red, *scal;
+  int* flags;
+
+  __device__ void bind(unsigned char* base, const AlLayout& l) {
+    L = l;
+    sc = reinterpret_cast<TrajScene<R>*>(base + L.scene);
+    x = reinterpret_cast<R*>(base + L.x);
+    g = reinterpret_cast<R*>(base + L.g);
+    unit = reinterpret_cast<R*>(base + L.unit);
+    ee = reinterpret_cast<R*>(base + L.ee);
+    rot = reinterpret_cast<R*>(base + L.rot);
+    armw = reinterpret_cast<R*>(base + L.armw);
+    ga = reinterpret_cast<R*>(base + L.ga);
+    hp = reinterpret_cast<R*>(base + L.hp);
+    gh = reinterpret_cast<R*>(base + L.gh);
+    pg = reinterpret_cast<R*>(base + L.pg);
+    pl = reinterpret_cast<R*>(base + L.pl);
+    psi = reinterpret_cast<R*>(base + L.seg);
+    cp = psi + L.B;
+    sp = cp + L.B;
+    rows = reinterpret_cast<R*>(base + L.rows);
+    gpose = reinterpret_cast<R*>(base + L.gpose);
+    scr = reinterpret_cast<R*>(base + L.scr);
+    pgsum = reinterpret_cast<R*>(base + L.pgsum);
+    red = reinterpret_cast<R*>(base + L.red);
+    scal = reinterpret_cast<R*>(base + L.scal);
+    flags = reinterpret_cast<int*>(base + L.flags);
+  }
+};
+
+// penetration of one sphere pair; returns the (linear or squared) value and, when active,
+// the unscaled slope (d value / d ca = -slope * (ca - cb)) (trajopt.py:396-413)
+template <typename R>
+__device__ __forceinline__ R pen_term(R dx, R dy, R dz, R rsum, bool quad, R* slope) {
+  const R d = Math<R>::sqrt_((dx * dx + dy * dy) + dz * dz);
+  R pen = rsum - d;
+  pen = pen > R(0) ? pen : R(0);
+  const bool live = pen > R(0) && d > R(0);
+  *slope = live ? (quad ? R(2) * pen / d : R(1) / d) : R(0);
+  return quad ? pen * pen : pen;
+}
+
+// accumulate one sphere (centre c, radius r) against fixed obstacles: statics + staged
+// spheres [f0, f1); returns the summed value, adds the unscaled gradient to g
+template <typename R>
+__device__ __forceinline__ R pens_fixed(const TrajScene<R>& sc, const R* c, R r, int f0, int f1, bool quad, R* g) {
+  R v = R(0);
+  for (int o = 0; o < sc.n_static; ++o) {
+    const R dx = c[0] - sc.st_c[o][0], dy = c[1] - sc.st_c[o][1], dz = c[2] - sc.st_c[o][2];
+    R sl;
+    v += pen_term(dx, dy, dz, r + sc.st_r[o], quad, &sl);
+    g[0] -= sl * dx;
+    g[1] -= sl * dy;
+    g[2] -= sl * dz;
+  }
+  for (int o = f0; o < f1; ++o) {
+    const R dx = c[0] - sc.staged[o][0], dy = c[1] - sc.staged[o][1], dz = c[2] - sc.staged[o][2];
+    R sl;
+    v += pen_term(dx, dy, dz, r + sc.br[o], quad, &sl);
+    g[0] -= sl * dx;
+    g[1] -= sl * dy;
+    g[2] -= sl * dz;
+  }
+  return v;
+}
+
+// Per-step state a waypoint tile carries across the phases (registers).
+template <typename R>
+struct WpState {
+  R z[3], o[3], ee[3], Ree[9];
+  R garm, gblk;       // unscaled joint gradients of the arm / held penetration sums
+  R d0[3], fac, dy0;  // start-alignment terms (t == 0)
+};
+
+// ---------------------------------------------------------------------------------------
+// al_eval: evaluate the AL objective, constraints and (want_grad) gradient of the CTA's
+// particle. With lr > 0 the clamped descent step (trajopt.py:993-1002) is applied to x in
+// place; otherwise (want_grad) the gradient is left in g[w*8 + k]. Ends with a barrier.
+// ---------------------------------------------------------------------------------------
+template <typename R, int KIND, int SPB>
+__device__ void al_eval(AlCtx<R>& C, const typename TwinSceneOf<R, KIND>::type& tw, const AlParams& prm, bool quad,
+                        bool pquad, bool want_grad, R lr) {
+  const TrajScene<R>& sc = *C.sc;
+  const ChainDesc<R>& ch = sc.ch;
+  const int tid = threadIdx.x;
+  const int W = C.L.W, J = ch.J, T = prm.T, B = sc.B, S = ch.S, SBn = C.L.SB;
+  const bool manip = sc.manip != 0;
+  const bool is_aux = tid >= C.L.NW;
+  const int lane = tid & 31;
+  const int w = tid >> 3;
+  const bool is_wp = !is_aux && w < W;
+  const Tile tl = Tile::make();
+  const int j = tl.j;
+  const int b = is_wp ? w / T : 0;
+  const int t = is_wp ? w - b * T : 0;
+  const bool interior = manip && t >= 1 && t <= T - 2;
+  const int h0 = manip ? sc.blk_start[b] : 0;
+  const int nh = manip ? sc.blk_start[b + 1] - h0 : 0;
+  const int f0 = manip ? sc.blk_start[b + 1] : 0, f1 = manip ? sc.n_blk : 0;
+  const R w_start = R(prm.w_start);
+  WpState<R> st;
+  R obj_w = R(0), carm = R(0), cblk = R(0);
+
+  // ---------------- P1: tile FK, sphere centres, leg, start terms ------------------------
+  if (!is_aux && w < C.L.NW / kTile) {
+    const int wq = is_wp ? w : 0;  // padding tiles mirror waypoint 0 (no writes)
+    const R qj = j < J ? C.x[wq * kXS + j] : R(0);
+    TileFrame<R> f;
+    tile_fk(tl, ch, qj, f);
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      st.z[c] = f.z[c];
+      st.o[c] = f.o[c];
+      st.ee[c] = f.ee[c];
+    }
+#pragma unroll
+    for (int c = 0; c < 9; ++c) st.Ree[c] = f.Ree[c];
+    if (is_wp) {
+      if (j == 0) {
+#pragma unroll
+        for (int c = 0; c < 3; ++c) C.ee[w * 3 + c] = f.ee[c];
+#pragma unroll
+        for (int c = 0; c < 9; ++c) C.rot[w * 9 + c] = f.Ree[c];
+      }
+      if (j < J)
+        for (int s = ch.link_start[j]; s < ch.link_start[j + 1]; ++s) tile_sphere(ch, f, s, C.armw + (w * S + s) * 3);
+      if (interior) {  // held block = Ree @ FLIP @ u + ee (trajopt.py:441-447)
+        for (int s = j; s < nh; s += kTile) {
+          const R ux = sc.bu[h0 + s][0], uy = sc.bu[h0 + s][1], uz = sc.bu[h0 + s][2];
+          R* h = C.hp + (w * SBn + s) * 3;
+          h[0] = ((f.Ree[0] * ux - f.Ree[1] * uy) - f.Ree[2] * uz) + f.ee[0];
+          h[1] = ((f.Ree[3] * ux - f.Ree[4] * uy) - f.Ree[5] * uz) + f.ee[1];
+          h[2] = ((f.Ree[6] * ux - f.Ree[7] * uy) - f.Ree[8] * uz) + f.ee[2];
+        }
+      }
+    }
+    // path length (trajopt.py:474-476): tile sum of the leg's squared components
+    R dv = R(0);
+    if (is_wp && t < T - 1 && j < J) dv = C.x[(wq + 1) * kXS + j] - qj;
+    const R s2 = tl.sum(dv * dv);
+    if (is_wp && t < T - 1) {
+      const R ln = Math<R>::sqrt_(s2);
+      if (j == 0) obj_w += ln;
+      C.unit[w * kXS + j] = (ln > R(1e-12) && j < J) ? dv / ln : R(0);
+    }
+    // start alignment (trajopt.py:477-494), uniform across the tile
+    if (is_wp && manip && t == 0) {
+      st.d0[0] = f.ee[0] - sc.pick_pos[b][0];
+      st.d0[1] = f.ee[1] - sc.pick_pos[b][1];
+      st.d0[2] = f.ee[2] - sc.pick_pos[b][2];
+      R cosd = -f.Ree[8];
+      cosd = cosd < R(-1) ? R(-1) : (cosd > R(1) ? R(1) : cosd);
+      const R th = Math<R>::acos_(cosd);
+      st.dy0 = wrap_yaw(yaw_of(f.Ree) - sc.pick_yaw[b]);
+      const R sth = Math<R>::sqrt_(fmax(R(1) - cosd * cosd, R(0)));
+      st.fac = sth > R(1e-8) ? R(-2) * th / fmax(sth, R(1e-8)) : (cosd > R(0) ? R(-2) : R(0));
+      if (j == 0)
+        obj_w += w_start * ((((st.d0[0] * st.d0[0] + st.d0[1] * st.d0[1]) + st.d0[2] * st.d0[2]) + th * th) +
+                            st.dy0 * st.dy0);
+    }
+  }
+  __syncthreads();
+
+  // ---------------- P2: aux = placed poses + placement twin; tiles = fixed obstacles ----
+  if (is_aux) {
+    if (manip) {
+      if (lane < B) {
+        const int bb = lane, wf = bb * T + T - 1;
+        const R* Rf = C.rot + wf * 9;
+        const R* ef = C.ee + wf * 3;
+        const R ps = yaw_of(Rf) - sc.grasp_yaw;
+        R s, c;
+        Math<R>::sincos_(ps, &s, &c);
+        C.psi[bb] = ps;
+        C.cp[bb] = c;
+        C.sp[bb] = s;
+        const R ox = sc.grasp_off[0], oy = sc.grasp_off[1], oz = sc.grasp_off[2];
+        C.rows[4 * bb + 0] = ef[0] - (c * ox - s * oy);
+        C.rows[4 * bb + 1] = ef[1] - (s * ox + c * oy);
+        C.rows[4 * bb + 2] = ef[2] - oz;
+        C.rows[4 * bb + 3] = ps;
+        for (int q = sc.blk_start[bb]; q < sc.blk_start[bb + 1]; ++q) {
+          const R ux = sc.bu[q][0], uy = sc.bu[q][1], uz = sc.bu[q][2];
+          C.pl[3 * q + 0] = ef[0] + c * ux - s * uy;
+          C.pl[3 * q + 1] = ef[1] + s * ux + c * uy;
+          C.pl[3 * q + 2] = ef[2] + uz;
+        }
+      }
+      __syncwarp();
+      if (lane == 0) {
+        R cpl = twin_run<R, KIND, SPB>(tw, C.rows, C.gpose, C.scr, want_grad, pquad);
+        if (sc.anchor) {
+          for (int bb = 0; bb < B; ++bb) {
+            const R wp = wrap_yaw(C.psi[bb]);
+            cpl += pquad ? wp * wp : fabs(wp);
+            if (want_grad) C.gpose[4 * bb + 3] += pquad ? R(2) * wp : (wp > R(0) ? R(1) : (wp < R(0) ? R(-1) : R(0)));
+          }
+        }
+        C.scal[kCplace] = cpl;
+      }
+    }
+  } else if (is_wp) {
+    if (j < J) {
+      for (int s = ch.link_start[j]; s < ch.link_start[j + 1]; ++s) {
+        R gg[3] = {R(0), R(0), R(0)};
+        carm += pens_fixed(sc, C.armw + (w * S + s) * 3, ch.arm_r[s], f0, f1, quad, gg);
+        R* ga = C.ga + (w * S + s) * 3;
+        ga[0] = gg[0];
+        ga[1] = gg[1];
+        ga[2] = gg[2];
+      }
+    }
+    if (interior) {
+      for (int s = j; s < nh; s += kTile) {
+        R gg[3] = {R(0), R(0), R(0)};
+        cblk += pens_fixed(sc, C.hp + (w * SBn + s) * 3, sc.br[h0 + s], f0, f1, quad, gg);
+        R* gh = C.gh + (w * SBn + s) * 3;
+        gh[0] = gg[0];
+        gh[1] = gg[1];
+        gh[2] = gg[2];
+      }
+    }
+  }
+  __syncthreads();
+
+  // ---------------- P3: placed blocks, placed-pose partials, J^T products ------------------
+  st.garm = R(0);
+  st.gblk = R(0);
+  if (!is_aux && w < C.L.NW / kTile) {
+    if (manip && is_wp) {
+      for (int jb = 0; jb < b; ++jb) {
+        const R cj = C.cp[jb], sj = C.sp[jb];
+        R A[4] = {R(0), R(0), R(0), R(0)}, H[4] = {R(0), R(0), R(0), R(0)};
+        for (int q = sc.blk_start[jb]; q < sc.blk_start[jb + 1]; ++q) {
+          const R px = C.pl[3 * q], py = C.pl[3 * q + 1], pz = C.pl[3 * q + 2], rq = sc.br[q];
+          const R drx = -sj * sc.bu[q][0] - cj * sc.bu[q][1];
+          const R dry = cj * sc.bu[q][0] - sj * sc.bu[q][1];
+          if (j < J) {
+            for (int s = ch.link_start[j]; s < ch.link_start[j + 1]; ++s) {
+              const R* a = C.armw + (w * S + s) * 3;
+              const R dx = a[0] - px, dy = a[1] - py, dz = a[2] - pz;
+              R sl;
+              carm += pen_term(dx, dy, dz, ch.arm_r[s] + rq, quad, &sl);
+              if (want_grad && sl != R(0)) {
+                R* ga = C.ga + (w * S + s) * 3;
+                ga[0] -= sl * dx;
+                ga[1] -= sl * dy;
+                ga[2] -= sl * dz;
+                A[0] += sl * dx;
+                A[1] += sl * dy;
+                A[2] += sl * dz;
+                A[3] += (sl * dx) * drx + (sl * dy) * dry;
+              }
+            }
+          }
+          if (interior) {
+            for (int s = j; s < nh; s += kTile) {
+              const R* h = C.hp + (w * SBn + s) * 3;
+              const R dx = h[0] - px, dy = h[1] - py, dz = h[2] - pz;
+              R sl;
+              cblk += pen_term(dx, dy, dz, sc.br[h0 + s] + rq, quad, &sl);
+              if (want_grad && sl != R(0)) {
+                R* gh = C.gh + (w * SBn + s) * 3;
+                gh[0] -= sl * dx;
+                gh[1] -= sl * dy;
+                gh[2] -= sl * dz;
+                H[0] += sl * dx;
+                H[1] += sl * dy;
+                H[2] += sl * dz;
+                H[3] += (sl * dx) * drx + (sl * dy) * dry;
+              }
+            }
+          }
+        }
+        if (want_grad) {  // tile-reduce, lane 0 stores [class][block jb][G xyz | G yaw]
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const R av = tl.sum(A[i]), hv = tl.sum(H[i]);
+            if (j == 0) {
+              C.pg[((w * 2 + 0) * B + jb) * 4 + i] = av;
+              C.pg[((w * 2 + 1) * B + jb) * 4 + i] = hv;
+            }
+          }
+        }
+      }
+    }
+    if (want_grad) {
+      // arm: suffix sums over links >= k of (g, a x g), lane k = joint k (trajopt.py:586-590)
+      R G[3] = {R(0), R(0), R(0)}, Mv[3] = {R(0), R(0), R(0)};
+      if (is_wp && j < J) {
+        for (int s = ch.link_start[j]; s < ch.link_start[j + 1]; ++s) {
+          const R* a = C.armw + (w * S + s) * 3;
+          const R* gg = C.ga + (w * S + s) * 3;
+          R m[3];
+          cross3(a, gg, m);
+          G[0] += gg[0];
+          G[1] += gg[1];
+          G[2] += gg[2];
+          Mv[0] += m[0];
+          Mv[1] += m[1];
+          Mv[2] += m[2];
+        }
+      }
+#pragma unroll
+      for (int d = 1; d < kTile; d <<= 1) {
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          const R gv = tl.down(G[c], d), mv = tl.down(Mv[c], d);
+          if (j + d < kTile) {
+            G[c] += gv;
+            Mv[c] += mv;
+          }
+        }
+      }
+      R og[3];
+      cross3(st.o, G, og);
+      st.garm = (st.z[0] * (Mv[0] - og[0]) + st.z[1] * (Mv[1] - og[1])) + st.z[2] * (Mv[2] - og[2]);
+      // held block: every joint moves it (trajopt.py:592-599)
+      R Gh[3] = {R(0), R(0), R(0)}, Mh[3] = {R(0), R(0), R(0)};
+      if (interior && is_wp) {
+        for (int s = j; s < nh; s += kTile) {
+          const R* a = C.hp + (w * SBn + s) * 3;
+          const R* gg = C.gh + (w * SBn + s) * 3;
+          R m[3];
+          cross3(a, gg, m);
+          Gh[0] += gg[0];
+          Gh[1] += gg[1];
+          Gh[2] += gg[2];
+          Mh[0] += m[0];
+          Mh[1] += m[1];
+          Mh[2] += m[2];
+        }
+      }
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        Gh[c] = tl.sum(Gh[c]);
+        Mh[c] = tl.sum(Mh[c]);
+      }
+      cross3(st.o, Gh, og);
+      st.gblk = (st.z[0] * (Mh[0] - og[0]) + st.z[1] * (Mh[1] - og[1])) + st.z[2] * (Mh[2] - og[2]);
+    }
+  }
+  // warp partial sums of the scalars (fixed xor-tree order)
+  if (!is_aux) {
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      obj_w += __shfl_xor_sync(0xffffffffu, obj_w, off);
+      carm += __shfl_xor_sync(0xffffffffu, carm, off);
+      cblk += __shfl_xor_sync(0xffffffffu, cblk, off);
+    }
+    if (lane == 0) {
+      C.red[4 * (tid >> 5) + 0] = obj_w;
+      C.red[4 * (tid >> 5) + 1] = carm;
+      C.red[4 * (tid >> 5) + 2] = cblk;
+    }
+  }
+  __syncthreads();
+
+  // ---------------- P4: totals, multiplier scales; aux reduces placed partials ----------
+  if (tid == 0) {
+    R o = R(0), ca = R(0), cb = R(0);
+    for (int wi = 0; wi < C.L.NW / 32; ++wi) {
+      o += C.red[4 * wi];
+      ca += C.red[4 * wi + 1];
+      cb += C.red[4 * wi + 2];
+    }
+    const R cpl = manip ? C.scal[kCplace] : R(0);
+    const R c0 = R(prm.w_place) * cpl, c1 = R(prm.w_arm) * ca, c2 = R(prm.w_block) * cb;
+    const R mu = C.scal[kMu];
+    const R l0 = C.scal[kLam0], l1 = C.scal[kLam1], l2 = C.scal[kLam2];
+    C.scal[kObj] = o;
+    C.scal[kCarm] = ca;
+    C.scal[kCblk] = cb;
+    C.scal[kCons0] = c0;
+    C.scal[kCons1] = c1;
+    C.scal[kCons2] = c2;
+    C.scal[kLag] = o + ((l0 * c0 + l1 * c1) + l2 * c2) + R(0.5) * mu * ((c0 * c0 + c1 * c1) + c2 * c2);
+    C.scal[kSc0] = (l0 + mu * c0) * R(prm.w_place);
+    C.scal[kSc1] = (l1 + mu * c1) * R(prm.w_arm);
+    C.scal[kSc2] = (l2 + mu * c2) * R(prm.w_block);
+  }
+  if (want_grad && manip && is_aux) {
+    for (int it = lane; it < 8 * B; it += 32) {
+      const int cls = it / (4 * B), jb = (it / 4) % B, i = it % 4;
+      R s = R(0);
+      for (int wv = (jb + 1) * T; wv < W; ++wv) s += C.pg[((wv * 2 + cls) * B + jb) * 4 + i];
+      C.pgsum[it] = s;
+    }
+  }
+  __syncthreads();
+
+  // ---------------- P5: gradient assembly (lane k = joint k) + optional update -----------
+  if (want_grad && is_wp && j < J) {
+    const R s_pl = C.scal[kSc0], s_arm = C.scal[kSc1], s_blk = C.scal[kSc2];
+    R gq = R(0);
+    if (t < T - 1) gq -= C.unit[w * kXS + j];
+    if (t >= 1) gq += C.unit[(w - 1) * kXS + j];
+    gq += s_arm * st.garm;
+    gq += s_blk * st.gblk;
+    if (manip && t == T - 1) {  // placement chain (trajopt.py:601-635)
+      const R ox = sc.grasp_off[0], oy = sc.grasp_off[1];
+      const R c = C.cp[b], s = C.sp[b];
+      const R dox = s * ox + c * oy, doy = -c * ox + s * oy;
+      const R gp0 = s_pl * C.gpose[4 * b], gp1 = s_pl * C.gpose[4 * b + 1], gp2 = s_pl * C.gpose[4 * b + 2],
+              gp3 = s_pl * C.gpose[4 * b + 3];
+      const R gyp = (gp0 * dox + gp1 * doy) + gp3;
+      const R Gx = s_arm * C.pgsum[(0 * B + b) * 4 + 0] + s_blk * C.pgsum[(1 * B + b) * 4 + 0];
+      const R Gy = s_arm * C.pgsum[(0 * B + b) * 4 + 1] + s_blk * C.pgsum[(1 * B + b) * 4 + 1];
+      const R Gz = s_arm * C.pgsum[(0 * B + b) * 4 + 2] + s_blk * C.pgsum[(1 * B + b) * 4 + 2];
+      const R Gw = s_arm * C.pgsum[(0 * B + b) * 4 + 3] + s_blk * C.pgsum[(1 * B + b) * 4 + 3];
+      const R rel[3] = {st.ee[0] - st.o[0], st.ee[1] - st.o[1], st.ee[2] - st.o[2]};
+      R jl[3];
+      cross3(st.z, rel, jl);
+      gq += ((Gx + gp0) * jl[0] + (Gy + gp1) * jl[1]) + (Gz + gp2) * jl[2];
+      gq += (Gw + gyp) * yaw_jac(st.Ree, st.z);
+    }
+    if (manip && t == 0) {  // start alignment (trajopt.py:637-651)
+      const R ax0[3] = {st.Ree[2], st.Ree[5], st.Ree[8]};
+      const R rel[3] = {st.ee[0] - st.o[0], st.ee[1] - st.o[1], st.ee[2] - st.o[2]};
+      R jl[3], dc[3];
+      cross3(st.z, rel, jl);
+      cross3(st.z, ax0, dc);
+      gq += w_start * R(2) * ((st.d0[0] * jl[0] + st.d0[1] * jl[1]) + st.d0[2] * jl[2]);
+      gq += w_start * st.fac * (-dc[2]);
+      gq += w_start * R(2) * st.dy0 * yaw_jac(st.Ree, st.z);
+    }
+    if (lr > R(0)) {  // x <- clip(x - clip(lr g, +-0.1), lower, upper) (trajopt.py:997-1002)
+      R stp = lr * gq;
+      stp = stp < R(-0.1) ? R(-0.1) : (stp > R(0.1) ? R(0.1) : stp);
+      R v = C.x[w * kXS + j] - stp;
+      v = v < ch.lo[j] ? ch.lo[j] : (v > ch.hi[j] ? ch.hi[j] : v);
+      if (!manip) {
+        if (w == 0) v = sc.start[j];
+        if (w == T - 1) v = sc.goal[j];
+      }
+      C.x[w * kXS + j] = v;
+    } else {
+      C.g[w * kXS + j] = gq;
+    }
+  }
+  __syncthreads();
+}
+
+// ---------------------------------------------------------------------------------------
+// validation of the CTA's particle (trajopt.py:1071-1153). Requires ee/rot/armw/hp of the
+// current x (a preceding al_eval). Leaves the max violation in scal[kWorst].
+// ---------------------------------------------------------------------------------------
+template <typename R, int KIND, int SPB>
+__device__ void al_validate(AlCtx<R>& C, const typename TwinSceneOf<R, KIND>::type& tw, const AlParams& prm) {
+  const TrajScene<R>& sc = *C.sc;
+  const ChainDesc<R>& ch = sc.ch;
+  const int tid = threadIdx.x;
+  const int W = C.L.W, J = ch.J, T = prm.T, B = sc.B, S = ch.S, SBn = C.L.SB;
+  const bool manip = sc.manip != 0;
+  const bool is_aux = tid >= C.L.NW;
+  const int lane = tid & 31;
+  const int w = tid >> 3;
+  const bool is_wp = !is_aux && w < W;
+  const int j = tid & 7;
+  const int b = is_wp ? w / T : 0;
+  const int t = is_wp ? w - b * T : 0;
+  // placed blocks from the final waypoints: inverse_grasp of the wrapped EE pose
+  if (is_aux && manip && lane < B) {
+    const int bb = lane, wf = bb * T + T - 1;
+    const R* Rf = C.rot + wf * 9;
+    const R* ef = C.ee + wf * 3;
+    const R yaw = wrap_yaw(wrap_yaw(yaw_of(Rf)) - sc.grasp_yaw);
+    R s, c;
+    Math<R>::sincos_(yaw, &s, &c);
+    const R ox = sc.grasp_off[0], oy = sc.grasp_off[1], oz = sc.grasp_off[2];
+    const R px = ef[0] - (c * ox - s * oy), py = ef[1] - (s * ox + c * oy), pz = ef[2] - oz;
+    C.rows[4 * bb + 0] = px;
+    C.rows[4 * bb + 1] = py;
+    C.rows[4 * bb + 2] = pz;
+    C.rows[4 * bb + 3] = yaw;
+    for (int q = sc.blk_start[bb]; q < sc.blk_start[bb + 1]; ++q) {
+      const R lx = sc.bu[q][0] + ox, ly = sc.bu[q][1] + oy, lz = sc.bu[q][2] + oz;
+      C.pl[3 * q + 0] = (lx * c - ly * s) + px;
+      C.pl[3 * q + 1] = (lx * s + ly * c) + py;
+      C.pl[3 * q + 2] = lz + pz;
+    }
+  }
+  __syncthreads();
+  R worst = R(0);
+  if (is_aux && lane == 0) {
+    if (manip) {
+      R place = twin_run<R, KIND, SPB>(tw, C.rows, nullptr, C.scr, false, false);
+      if (sc.anchor)
+        for (int bb = 0; bb < B; ++bb) place += fabs(wrap_yaw(C.rows[4 * bb + 3]));
+      worst = fmax(worst, place);
+    } else {
+      for (int k = 0; k < J; ++k) {
+        worst = fmax(worst, fabs(C.x[0 * kXS + k] - sc.start[k]));
+        worst = fmax(worst, fabs(C.x[(T - 1) * kXS + k] - sc.goal[k]));
+      }
+    }
+  } else if (is_wp) {
+    if (j < J) {
+      const R q = C.x[w * kXS + j];
+      worst = fmax(worst, fmax(q - ch.hi[j], ch.lo[j] - q));
+    }
+    const int f0 = manip ? sc.blk_start[b + 1] : 0, f1 = manip ? sc.n_blk : 0;
+    const int p_end = manip ? sc.blk_start[b] : 0;  // placed spheres of blocks j < b
+    const bool any_obs = (sc.n_static + (f1 - f0) + p_end) > 0;
+    if (any_obs) {
+      auto check = [&](const R* c, R r) {
+        for (int o = 0; o < sc.n_static; ++o) {
+          const R dx = c[0] - sc.st_c[o][0], dy = c[1] - sc.st_c[o][1], dz = c[2] - sc.st_c[o][2];
+          worst = fmax(worst, (r + sc.st_r[o]) - Math<R>::sqrt_((dx * dx + dy * dy) + dz * dz));
+        }
+        for (int o = f0; o < f1; ++o) {
+          const R dx = c[0] - sc.staged[o][0], dy = c[1] - sc.staged[o][1], dz = c[2] - sc.staged[o][2];
+          worst = fmax(worst, (r + sc.br[o]) - Math<R>::sqrt_((dx * dx + dy * dy) + dz * dz));
+        }
+        for (int o = 0; o < p_end; ++o) {
+          const R dx = c[0] - C.pl[3 * o], dy = c[1] - C.pl[3 * o + 1], dz = c[2] - C.pl[3 * o + 2];
+          worst = fmax(worst, (r + sc.br[o]) - Math<R>::sqrt_((dx * dx + dy * dy) + dz * dz));
+        }
+      };
+      if (j < J)
+        for (int s = ch.link_start[j]; s < ch.link_start[j + 1]; ++s) check(C.armw + (w * S + s) * 3, ch.arm_r[s]);
+      if (manip && t >= 1 && t <= T - 2) {
+        const int h0 = sc.blk_start[b], nh = sc.blk_start[b + 1] - h0;
+        for (int s = j; s < nh; s += kTile) check(C.hp + (w * SBn + s) * 3, sc.br[h0 + s]);
+      }
+    }
+    if (manip && t == 0 && j == 0) {
+      const R* Rm = C.rot + w * 9;
+      const R dx = C.ee[w * 3] - sc.pick_pos[b][0], dy = C.ee[w * 3 + 1] - sc.pick_pos[b][1],
+              dz = C.ee[w * 3 + 2] - sc.pick_pos[b][2];
+      worst = fmax(worst, Math<R>::sqrt_((dx * dx + dy * dy) + dz * dz));
+      worst = fmax(worst, fabs(wrap_yaw(wrap_yaw(yaw_of(Rm)) - sc.pick_yaw[b])));
+      R cd = -Rm[8];
+      cd = cd < R(-1) ? R(-1) : (cd > R(1) ? R(1) : cd);
+      worst = fmax(worst, Math<R>::acos_(cd));
+    }
+  }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) worst = fmax(worst, __shfl_xor_sync(0xffffffffu, worst, off));
+  if (lane == 0) C.red[4 * (tid >> 5) + 3] = worst;
+  __syncthreads();
+  if (tid == 0) {
+    R wv = R(0);
+    for (int wi = 0; wi < C.L.nwarps; ++wi) wv = fmax(wv, C.red[4 * wi + 3]);
+    C.scal[kWorst] = wv;
+  }
+  __syncthreads();
+}
+
+// load the trajectory scene + particle p into shared memory (x rows [w][8])
+template <typename R>
+__device__ void al_load(AlCtx<R>& C, const TrajScene<R>* g_scene, const R* values, int64_t p) {
+  const int tid = threadIdx.x;
+  {
+    const int4* src = reinterpret_cast<const int4*>(g_scene);
+    int4* dst = reinterpret_cast<int4*>(C.sc);
+    const int n = (int)(sizeof(TrajScene<R>) / sizeof(int4));
+    for (int i = tid; i < n; i += blockDim.x) dst[i] = src[i];
+  }
+  const int W = C.L.W, J = C.L.J;
+  const R* v = values + p * (int64_t)W * J;
+  for (int i = tid; i < W * kXS; i += blockDim.x) {
+    const int w = i / kXS, k = i - w * kXS;
+    C.x[i] = k < J ? v[w * J + k] : R(0);
+  }
+  if (tid < 32) C.scal[tid] = R(0);
+  __syncthreads();
+}
+
+template <typename R>
+__device__ void al_store_x(const AlCtx<R>& C, R* dst) {
+  const int W = C.L.W, J = C.L.J;
+  for (int i = threadIdx.x; i < W * J; i += blockDim.x) {
+    const int w = i / J, k = i - w * J;
+    dst[i] = C.x[w * kXS + k];
+  }
+}
+
+// ---------------------------------------------------------------------------------------
+// k_al_eval: trajectory_cost / al_value_and_gradient for a batch (CTA per particle)
+// ---------------------------------------------------------------------------------------
+template <typename R, int KIND, int SPB>
+__global__ void __launch_bounds__(kMaxAlThreads) k_al_eval(const TrajScene<R>* __restrict__ g_scene,
+                                                           const typename TwinSceneOf<R, KIND>::type tw, AlLayout L,
+                                                           AlParams prm, const R* __restrict__ values,
+                                                           const R* __restrict__ lam, const R* __restrict__ mu,
+                                                           int mode, int place_mode, int want_grad,
+                                                           R* __restrict__ obj, R* __restrict__ cons,
+                                                           R* __restrict__ lag, R* __restrict__ grad) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  AlCtx<R> C;
+  C.bind(smem, L);
+  const int64_t p = blockIdx.x;
+  al_load(C, g_scene, values, p);
+  if (threadIdx.x == 0) {
+    C.scal[kLam0] = lam ? lam[3 * p] : R(0);
+    C.scal[kLam1] = lam ? lam[3 * p + 1] : R(0);
+    C.scal[kLam2] = lam ? lam[3 * p + 2] : R(0);
+    C.scal[kMu] = mu ? mu[p] : R(0);
+  }
+  __syncthreads();
+  al_eval<R, KIND, SPB>(C, tw, prm, mode == 1, place_mode == 1, want_grad != 0, R(0));
+  if (threadIdx.x == 0) {
+    if (obj) obj[p] = C.scal[kObj];
+    if (cons) {
+      cons[3 * p] = C.scal[kCons0];
+      cons[3 * p + 1] = C.scal[kCons1];
+      cons[3 * p + 2] = C.scal[kCons2];
+    }
+    if (lag) lag[p] = C.scal[kLag];
+  }
+  if (want_grad && grad) {
+    const int W = L.W, J = L.J;
+    R* gout = grad + p * (int64_t)W * J;
+    for (int i = threadIdx.x; i < W * J; i += blockDim.x) {
+      const int w = i / J, k = i - w * J;
+      gout[i] = C.g[w * kXS + k];
+    }
+  }
+}
+
+// k_validate: validate() for a batch of trajectories (CTA per trajectory)
+template <typename R, int KIND, int SPB>
+__global__ void __launch_bounds__(kMaxAlThreads) k_validate(const TrajScene<R>* __restrict__ g_scene,
+                                                            const typename TwinSceneOf<R, KIND>::type tw, AlLayout L,
+                                                            AlParams prm, const R* __restrict__ values,
+                                                            uint8_t* __restrict__ feasible,
+                                                            R* __restrict__ violation) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  AlCtx<R> C;
+  C.bind(smem, L);
+  const int64_t p = blockIdx.x;
+  al_load(C, g_scene, values, p);
+  al_eval<R, KIND, SPB>(C, tw, prm, false, false, false, R(0));  // FK tables for the current x
+  al_validate<R, KIND, SPB>(C, tw, prm);
+  if (threadIdx.x == 0) {
+    const R wv = C.scal[kWorst];
+    violation[p] = wv;
+    feasible[p] = (uint8_t)(wv < R(prm.eps));
+  }
+}
+
+// ---------------------------------------------------------------------------------------
+// k_solve_al: solve_al (trajopt.py:936-1063), one CTA per trajectory particle.
+//
+// Particles only interact through "stop at the first outer iteration in which ANY
+// particle validates". Each CTA publishes its first feasible outer with atomicMin on
+// *kstar and stops as soon as a lower-indexed outer has produced a feasible particle
+// (it has then recorded every outer <= kstar). Per-outer records and the snapshot at
+// the particle's first feasible outer make the final choice (lowest objective among
+// the particles feasible at kstar, first index on ties) independent of CTA timing.
+// ---------------------------------------------------------------------------------------
+struct AlRecords {
+  void *mu, *lam, *cons, *upd, *obj, *viol;  // [outer][P] (x3 for lam/cons/upd), dtype R
+  uint8_t* feas;                             // [outer][P]
+  int32_t* first_feas;                       // [P] first feasible outer or -1
+  int32_t* n_outers;                         // [P] outers completed
+  int* kstar;                                // global min feasible outer (INT_MAX = none yet)
+  void* best_x;                              // [P][B][T][J] snapshot at first feasible outer
+  const int32_t* n_active;                   // device count of live particles (nullptr = gridDim.x)
+};
+
+template <typename R, int KIND, int SPB>
+__global__ void __launch_bounds__(kMaxAlThreads) k_solve_al(const TrajScene<R>* __restrict__ g_scene,
+                                                            const typename TwinSceneOf<R, KIND>::type tw, AlLayout L,
+                                                            AlParams prm, const R* __restrict__ values, int P,
+                                                            AlRecords rec) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  AlCtx<R> C;
+  C.bind(smem, L);
+  const int p = blockIdx.x;
+  if (rec.n_active && p >= *rec.n_active) return;
+  al_load(C, g_scene, values, p);
+  const TrajScene<R>& sc = *C.sc;
+  const ChainDesc<R>& ch = sc.ch;
+  const int tid = threadIdx.x;
+  const int W = L.W, J = ch.J, T = prm.T;
+  const bool manip = sc.manip != 0;
+  R* r_mu = reinterpret_cast<R*>(rec.mu);
+  R* r_lam = reinterpret_cast<R*>(rec.lam);
+  R* r_cons = reinterpret_cast<R*>(rec.cons);
+  R* r_upd = reinterpret_cast<R*>(rec.upd);
+  R* r_obj = reinterpret_cast<R*>(rec.obj);
+  R* r_viol = reinterpret_cast<R*>(rec.viol);
+  if (tid == 0) {
+    C.scal[kMu] = R(prm.mu0);
+    C.scal[kPrev] = R(INFINITY);
+    C.flags[0] = 0;
+  }
+  __syncthreads();
+  const R denom = R(prm.inner_steps - 1 > 1 ? prm.inner_steps - 1 : 1);
+  int first = -1, done = 0;
+  for (int outer = 0; outer < prm.outer_iters; ++outer) {
+    if (tid == 0) C.flags[0] = (outer > *((volatile int*)rec.kstar)) ? 1 : 0;
+    __syncthreads();
+    if (C.flags[0]) break;
+    for (int k = 0; k < prm.inner_steps; ++k) {
+      const R lr = R(prm.lr_init) + (R(prm.lr_final) - R(prm.lr_init)) * (R(k) / denom);
+      al_eval<R, KIND, SPB>(C, tw, prm, false, prm.place_mode == 1, true, lr);
+    }
+    // retract pick waypoints to the exact grasp (trajopt.py:1004-1007): one 8-lane tile
+    // per segment, lane j = joint j
+    if (manip && (tid >> 3) < sc.B) {
+      const Tile tl = Tile::make();
+      const int bb = tid >> 3;
+      const int w0 = bb * T;
+      R qj = tl.j < J ? C.x[w0 * kXS + tl.j] : R(0);
+      tile_polish<R>(tl, ch, qj, sc.pick_pos[bb], sc.pick_yaw[bb]);
+      if (tl.j < J) C.x[w0 * kXS + tl.j] = qj;
+    }
+    __syncthreads();
+    al_eval<R, KIND, SPB>(C, tw, prm, false, prm.place_mode == 1, false, R(0));
+    al_validate<R, KIND, SPB>(C, tw, prm);
+    if (tid == 0) {
+      const int64_t o = (int64_t)outer * P + p;
+      const R mu = C.scal[kMu];
+      const R c0 = C.scal[kCons0], c1 = C.scal[kCons1], c2 = C.scal[kCons2];
+      const R l0 = C.scal[kLam0], l1 = C.scal[kLam1], l2 = C.scal[kLam2];
+      const R u0 = l0 + mu * c0, u1 = l1 + mu * c1, u2 = l2 + mu * c2;
+      const R worst = C.scal[kWorst];
+      const bool feas = worst < R(prm.eps);
+      r_mu[o] = mu;
+      r_lam[3 * o] = l0;
+      r_lam[3 * o + 1] = l1;
+      r_lam[3 * o + 2] = l2;
+      r_cons[3 * o] = c0;
+      r_cons[3 * o + 1] = c1;
+      r_cons[3 * o + 2] = c2;
+      r_upd[3 * o] = u0;
+      r_upd[3 * o + 1] = u1;
+      r_upd[3 * o + 2] = u2;
+      r_obj[o] = C.scal[kObj];
+      r_viol[o] = worst;
+      rec.feas[o] = (uint8_t)feas;
+      C.flags[1] = feas ? 1 : 0;
+      if (feas) {
+        atomicMin(rec.kstar, outer);
+      } else {
+        // lam <- lam + mu c; mu *= beta where max c > prev / 10 (trajopt.py:1051-1054)
+        C.scal[kLam0] = u0;
+        C.scal[kLam1] = u1;
+        C.scal[kLam2] = u2;
+        const R v = fmax(fmax(c0, c1), c2);
+        if (v > C.scal[kPrev] / R(10)) C.scal[kMu] = mu * R(prm.beta);
+        C.scal[kPrev] = v;
+      }
+    }
+    __syncthreads();
+    done = outer + 1;
+    if (C.flags[1]) {
+      first = outer;
+      al_store_x(C, reinterpret_cast<R*>(rec.best_x) + (int64_t)p * W * J);
+      break;
+    }
+  }
+  if (tid == 0) {
+    rec.first_feas[p] = first;
+    rec.n_outers[p] = done;
+  }
+}
+
+}  // namespace spasm

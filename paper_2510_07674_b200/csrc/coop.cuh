@@ -1,0 +1,256 @@
+// Tile-cooperative kinematics: one 8-lane tile owns one arm configuration, lane j owns
+// joint j (J <= 8). This replaces the serial joint chain with
+//   * Rodrigues rotations of all joints at once (robot.py:71-84),
+//   * an inclusive prefix product of the 3x3 rotations over the tile (Hillis-Steele,
+//     3 shuffle levels) and an inclusive prefix sum of the link translations,
+//   * lane-local Jacobian columns (robot.py:183-224; trajopt.py:737-756),
+//   * a butterfly (xor) reduction of the damped normal matrix J J^T + lambda I: every lane
+//     receives a bitwise identical matrix (IEEE addition is commutative), so the redundant
+//     per-lane Cholesky solve and the convergence tests are uniform across the tile.
+// Per-tile vs the reference's lock-step batches: converged IK rows are frozen by the
+// reference (dq = 0, clip is idempotent), so iterating each tile to its own convergence is
+// identical. The polish re-applies the full-circle wrap to finished rows while other rows
+// still iterate; that wrap is not idempotent in floating point, so finished polish rows can
+// differ by rounding.
+// Used by ik_solve_batch (robot.py:227-302), _polish_tool_down (trajopt.py:726-776), the
+// lift branch score (trajopt.py:779-787) and the AL waypoint frames.
+#pragma once
+#include "stage2.cuh"
+
+namespace spasm {
+
+constexpr int kTile = 8;
+
+struct Tile {
+  unsigned mask;  // the tile's 8 lanes within the warp
+  int j;          // lane index inside the tile = joint index
+  __device__ __forceinline__ static Tile make() {
+    Tile t;
+    const int lane = threadIdx.x & 31;
+    t.j = lane & (kTile - 1);
+    t.mask = 0xFFu << (lane & ~(kTile - 1));
+    return t;
+  }
+  template <typename R>
+  __device__ __forceinline__ R up(R v, int d) const { return __shfl_up_sync(mask, v, d, kTile); }
+  template <typename R>
+  __device__ __forceinline__ R down(R v, int d) const { return __shfl_down_sync(mask, v, d, kTile); }
+  template <typename R>
+  __device__ __forceinline__ R xr(R v, int d) const { return __shfl_xor_sync(mask, v, d, kTile); }
+  template <typename R>
+  __device__ __forceinline__ R bcast(R v, int src) const { return __shfl_sync(mask, v, src, kTile); }
+  template <typename R>
+  __device__ __forceinline__ R sum(R v) const {
+    v += xr(v, 1);
+    v += xr(v, 2);
+    v += xr(v, 4);
+    return v;
+  }
+  template <typename R>
+  __device__ __forceinline__ R max(R v) const {
+    v = fmax(v, xr(v, 1));
+    v = fmax(v, xr(v, 2));
+    v = fmax(v, xr(v, 4));
+    return v;
+  }
+};
+
+// Per-lane frame of joint j after a tile FK:
+//   M   rotation before joint j (product of joints < j)     -> axis z = M * axis_j
+//   P   rotation after joint j (product of joints <= j)      -> link frame of link j
+//   o   joint origin p_j = sum_{i<=j} M_i offset_i
+// and, uniform across the tile, the end effector ee / Ree.
+template <typename R>
+struct TileFrame {
+  R P[9];
+  R z[3];
+  R o[3];
+  R ee[3];
+  R Ree[9];
+};
+
+template <typename R>
+__device__ __forceinline__ void tile_fk(const Tile& tl, const ChainDesc<R>& ch, R qj, TileFrame<R>& f) {
+  const int J = ch.J;
+  const int j = tl.j;
+  const bool live = j < J;
+  R Rj[9];
+  if (live) {
+    rodrigues(ch.axis[j], qj, Rj);
+  } else {
+#pragma unroll
+    for (int k = 0; k < 9; ++k) Rj[k] = (k % 4 == 0) ? R(1) : R(0);
+  }
+  // inclusive prefix product P_j = R_0 R_1 ... R_j
+#pragma unroll
+  for (int k = 0; k < 9; ++k) f.P[k] = Rj[k];
+#pragma unroll
+  for (int d = 1; d < kTile; d <<= 1) {
+    R O[9];
+#pragma unroll
+    for (int k = 0; k < 9; ++k) O[k] = tl.up(f.P[k], d);
+    if (j >= d) {
+      R N[9];
+      mat3_mul(O, f.P, N);
+#pragma unroll
+      for (int k = 0; k < 9; ++k) f.P[k] = N[k];
+    }
+  }
+  // exclusive product M_j (identity for joint 0)
+  R M[9];
+#pragma unroll
+  for (int k = 0; k < 9; ++k) {
+    const R v = tl.up(f.P[k], 1);
+    M[k] = j == 0 ? ((k % 4 == 0) ? R(1) : R(0)) : v;
+  }
+  R t[3] = {R(0), R(0), R(0)};
+  if (live) {
+    mat3_vec(M, ch.offset[j], t);
+    mat3_vec(M, ch.axis[j], f.z);
+  } else {
+    f.z[0] = f.z[1] = f.z[2] = R(0);
+  }
+  // inclusive prefix sum of the translations -> joint origins
+#pragma unroll
+  for (int c = 0; c < 3; ++c) f.o[c] = t[c];
+#pragma unroll
+  for (int d = 1; d < kTile; d <<= 1) {
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      const R v = tl.up(f.o[c], d);
+      if (j >= d) f.o[c] = v + f.o[c];
+    }
+  }
+  // end effector from the last joint's frame (robot.py:136-141)
+  R Pf[9], pf[3];
+#pragma unroll
+  for (int k = 0; k < 9; ++k) Pf[k] = tl.bcast(f.P[k], J - 1);
+#pragma unroll
+  for (int c = 0; c < 3; ++c) pf[c] = tl.bcast(f.o[c], J - 1);
+  R tt[3];
+  mat3_vec(Pf, ch.tool_t, tt);
+  f.ee[0] = pf[0] + tt[0];
+  f.ee[1] = pf[1] + tt[1];
+  f.ee[2] = pf[2] + tt[2];
+  mat3_mul(Pf, ch.tool_R, f.Ree);
+}
+
+// world centre of arm sphere s (owned by link j = this lane): p_j + P_j * local_s
+template <typename R>
+__device__ __forceinline__ void tile_sphere(const ChainDesc<R>& ch, const TileFrame<R>& f, int s, R* c) {
+  R t[3];
+  mat3_vec(f.P, ch.arm_local[s], t);
+  c[0] = t[0] + f.o[0];
+  c[1] = t[1] + f.o[1];
+  c[2] = t[2] + f.o[2];
+}
+
+// One damped least-squares step on the tile: A = sum_j col_j col_j^T + damping I (xor
+// reduced, identical on every lane), Cholesky, dq_j = col_j . y, max|dq| <= 0.5.
+template <typename R, int NR>
+__device__ __forceinline__ R tile_dls(const Tile& tl, const R (&col)[NR], const R (&e)[NR], R damping) {
+  R A[NR * NR];
+#pragma unroll
+  for (int a = 0; a < NR; ++a)
+#pragma unroll
+    for (int b = 0; b <= a; ++b) {
+      const R v = tl.sum(col[a] * col[b]);
+      A[a * NR + b] = v + (a == b ? damping : R(0));
+      A[b * NR + a] = A[a * NR + b];
+    }
+  R y[NR];
+  chol_solve<R, NR>(A, e, y);
+  R dq = R(0);
+#pragma unroll
+  for (int a = 0; a < NR; ++a) dq += col[a] * y[a];
+  const R mx = tl.max(fabs(dq));
+  return dq * fmin(R(1), R(0.5) / fmax(mx, R(1e-12)));
+}
+
+// ik_solve_batch for one (target, restart) tile (robot.py:262-302). Lane j holds q_j;
+// returns ok and writes the score |pos err| + |yaw err| (uniform across the tile).
+template <typename R>
+__device__ bool tile_ik(const Tile& tl, const ChainDesc<R>& ch, R& qj, const R tp[3], R ty, int max_iters, R damping,
+                        R* score) {
+  const int j = tl.j;
+  const bool live = j < ch.J;
+  TileFrame<R> f;
+  for (int it = 0; it < max_iters; ++it) {
+    tile_fk(tl, ch, qj, f);
+    const R pe[3] = {tp[0] - f.ee[0], tp[1] - f.ee[1], tp[2] - f.ee[2]};
+    const R ye = wrap_yaw(ty - yaw_of(f.Ree));
+    const R pn = Math<R>::sqrt_((pe[0] * pe[0] + pe[1] * pe[1]) + pe[2] * pe[2]);
+    if (pn < R(kIkPosTol) && fabs(ye) < R(kIkYawTol)) break;
+    const R rel[3] = {f.ee[0] - f.o[0], f.ee[1] - f.o[1], f.ee[2] - f.o[2]};
+    R c[3];
+    cross3(f.z, rel, c);
+    const R col[4] = {c[0], c[1], c[2], f.z[2]};
+    const R e4[4] = {pe[0], pe[1], pe[2], ye};
+    const R dq = tile_dls<R, 4>(tl, col, e4, damping);
+    if (live) {
+      const R v = qj + dq;
+      qj = v < ch.lo[j] ? ch.lo[j] : (v > ch.hi[j] ? ch.hi[j] : v);
+    }
+  }
+  tile_fk(tl, ch, qj, f);
+  const R pe[3] = {tp[0] - f.ee[0], tp[1] - f.ee[1], tp[2] - f.ee[2]};
+  const R pn = Math<R>::sqrt_((pe[0] * pe[0] + pe[1] * pe[1]) + pe[2] * pe[2]);
+  const R ye = fabs(wrap_yaw(ty - yaw_of(f.Ree)));
+  *score = pn + ye;
+  return pn < R(kIkPosTol) && ye < R(kIkYawTol);
+}
+
+// _polish_tool_down for one configuration on a tile (trajopt.py:726-776)
+template <typename R>
+__device__ bool tile_polish(const Tile& tl, const ChainDesc<R>& ch, R& qj, const R tp[3], R ty) {
+  const int j = tl.j;
+  const bool live = j < ch.J;
+  const R cos_tol = R(0.99998750002604164);  // cos(0.005)
+  const R two_pi = R(6.283185307179586476925286766559);
+  TileFrame<R> f;
+  for (int it = 0; it < kPolishMaxIters; ++it) {
+    tile_fk(tl, ch, qj, f);
+    const R pe[3] = {tp[0] - f.ee[0], tp[1] - f.ee[1], tp[2] - f.ee[2]};
+    const R ye = wrap_yaw(ty - yaw_of(f.Ree));
+    const R ax[3] = {f.Ree[2], f.Ree[5], f.Ree[8]};
+    const R pn = Math<R>::sqrt_((pe[0] * pe[0] + pe[1] * pe[1]) + pe[2] * pe[2]);
+    if (pn < R(kIkPosTol) && fabs(ye) < R(kIkYawTol) && -ax[2] > cos_tol) break;
+    const R rel[3] = {f.ee[0] - f.o[0], f.ee[1] - f.o[1], f.ee[2] - f.o[2]};
+    R c[3], d[3];
+    cross3(f.z, rel, c);
+    cross3(f.z, ax, d);
+    const R col[5] = {c[0], c[1], c[2], live ? yaw_jac(f.Ree, f.z) : R(0), d[2]};
+    const R e5[5] = {pe[0], pe[1], pe[2], ye, R(-1) - ax[2]};
+    const R dq = tile_dls<R, 5>(tl, col, e5, R(kIkDamping));
+    if (live) {
+      R v = qj + dq;
+      if (ch.full_circle[j]) v = ch.lo[j] + np_mod_pos(v - ch.lo[j], two_pi);
+      qj = v < ch.lo[j] ? ch.lo[j] : (v > ch.hi[j] ? ch.hi[j] : v);
+    }
+  }
+  tile_fk(tl, ch, qj, f);
+  const R pe[3] = {tp[0] - f.ee[0], tp[1] - f.ee[1], tp[2] - f.ee[2]};
+  const R pn = Math<R>::sqrt_((pe[0] * pe[0] + pe[1] * pe[1]) + pe[2] * pe[2]);
+  return pn < R(kIkPosTol) && fabs(wrap_yaw(ty - yaw_of(f.Ree))) < R(kIkYawTol) && -f.Ree[8] > cos_tol;
+}
+
+// largest arm-sphere penetration (no clamp) against a sphere set (trajopt.py:779-787)
+template <typename R>
+__device__ R tile_arm_worst_pen(const Tile& tl, const ChainDesc<R>& ch, R qj, const R (*cen)[3], const R* rad, int n) {
+  TileFrame<R> f;
+  tile_fk(tl, ch, qj, f);
+  R worst = -INFINITY;
+  if (tl.j < ch.J) {
+    for (int s = ch.link_start[tl.j]; s < ch.link_start[tl.j + 1]; ++s) {
+      R c[3];
+      tile_sphere(ch, f, s, c);
+      for (int o = 0; o < n; ++o) {
+        const R dx = c[0] - cen[o][0], dy = c[1] - cen[o][1], dz = c[2] - cen[o][2];
+        worst = fmax(worst, (ch.arm_r[s] + rad[o]) - Math<R>::sqrt_((dx * dx + dy * dy) + dz * dz));
+      }
+    }
+  }
+  return tl.max(worst);
+}
+
+}  // namespace spasm

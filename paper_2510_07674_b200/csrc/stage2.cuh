@@ -7,15 +7,7 @@
 //   yaw_jac     exact d(tool yaw)/dq                               (robot.py:194-224)
 //   chol_solve  SPD solve for the 4x4 / 5x5 damped least-squares systems (robot.py:283,
 //               trajopt.py:759; numpy uses LU, both are exact to rounding for SPD A)
-//   ik_thread   one (target, restart) lane of ik_solve_batch       (robot.py:227-302)
-//   polish_thread  _polish_tool_down for one configuration          (trajopt.py:726-776)
-//
-// Per-thread semantics vs the reference's lock-step batches: converged IK rows are frozen
-// by the reference (dq = 0, clip is idempotent), so iterating each row to its own
-// convergence is identical. The polish re-applies the full-circle wrap to finished rows
-// while other rows of the batch still iterate; that wrap is not idempotent in floating
-// point, so finished rows can differ from the reference by rounding (<= 1 ulp per
-// remaining batch iteration). DESIGN.md records this.
+//   (the IK / polish iterations themselves are tile-cooperative: coop.cuh)
 #pragma once
 #include "rng.cuh"
 #include "scene.cuh"
@@ -28,6 +20,8 @@ constexpr int kMaxSeg = 8;        // segments (= blocks)
 constexpr int kMaxBlkS = 64;      // block spheres over all blocks
 constexpr int kMaxStat2 = 128;    // static obstacle spheres
 constexpr int kIkRestarts = 16;   // ik_solve_batch default restarts (robot.py:230)
+constexpr double kIkPosTol = 1e-4, kIkYawTol = 1e-3, kIkDamping = 1e-3;  // robot.py:22-24
+constexpr int kPolishMaxIters = 1000;                                     // trajopt.py:100
 
 template <typename R>
 struct alignas(16) ChainDesc {
@@ -235,148 +229,11 @@ __device__ __forceinline__ void chol_solve(R* A, const R* e, R* y) {
   }
 }
 
-// One damped-least-squares step: dq = Jm^T (Jm Jm^T + damping I)^-1 e, scaled so
-// max|dq| <= 0.5 (robot.py:281-287, trajopt.py:757-763).
-template <typename R, int NR>
-__device__ __forceinline__ void dls_step(const R (&Jm)[NR][kMaxJ], int J, const R* e, R damping, R* dq) {
-  R A[NR * NR];
-#pragma unroll
-  for (int i = 0; i < NR; ++i)
-#pragma unroll
-    for (int k = 0; k < NR; ++k) {
-      R s = R(0);
-#pragma unroll
-      for (int j = 0; j < kMaxJ; ++j)
-        if (j < J) s += Jm[i][j] * Jm[k][j];
-      A[i * NR + k] = s + (i == k ? damping : R(0));
-    }
-  R y[NR];
-  chol_solve<R, NR>(A, e, y);
-  R mx = R(0);
-#pragma unroll
-  for (int j = 0; j < kMaxJ; ++j) {
-    if (j >= J) break;
-    R s = R(0);
-#pragma unroll
-    for (int i = 0; i < NR; ++i) s += Jm[i][j] * y[i];
-    dq[j] = s;
-    mx = fmax(mx, fabs(s));
-  }
-  const R scale = fmin(R(1), R(0.5) / fmax(mx, R(1e-12)));
-#pragma unroll
-  for (int j = 0; j < kMaxJ; ++j)
-    if (j < J) dq[j] *= scale;
-}
-
 // FK returning origins/axes in registers (J <= kMaxJ), for the IK / polish lanes
 template <typename R>
 __device__ __forceinline__ void fk_frames(const ChainDesc<R>& ch, const R* q, R (&org)[kMaxJ][3], R (&axs)[kMaxJ][3],
                                           R ee[3], R Ree[9]) {
   fk_eval<R>(ch, q, 1, &org[0][0], &axs[0][0], nullptr, 1, ee, Ree);
-}
-
-constexpr double kIkPosTol = 1e-4, kIkYawTol = 1e-3, kIkDamping = 1e-3;
-constexpr int kPolishMaxIters = 1000;
-
-// ik_solve_batch for one (target, restart) lane (robot.py:262-302): iterate to convergence
-// (frozen thereafter, as the lock-step reference does) or max_iters, then the final check.
-// Returns ok, writes the score |pos err| + |yaw err|.
-template <typename R>
-__device__ bool ik_thread(const ChainDesc<R>& ch, R* q, const R tp[3], R ty, int max_iters, R damping, R* score) {
-  const int J = ch.J;
-  R org[kMaxJ][3], axs[kMaxJ][3], ee[3], Rm[9];
-  for (int it = 0; it < max_iters; ++it) {
-    fk_frames(ch, q, org, axs, ee, Rm);
-    const R pe[3] = {tp[0] - ee[0], tp[1] - ee[1], tp[2] - ee[2]};
-    const R ye = wrap_yaw(ty - yaw_of(Rm));
-    const R pn = Math<R>::sqrt_((pe[0] * pe[0] + pe[1] * pe[1]) + pe[2] * pe[2]);
-    if (pn < R(kIkPosTol) && fabs(ye) < R(kIkYawTol)) break;
-    R Jm[4][kMaxJ];
-#pragma unroll
-    for (int j = 0; j < kMaxJ; ++j) {
-      if (j >= J) break;
-      const R rel[3] = {ee[0] - org[j][0], ee[1] - org[j][1], ee[2] - org[j][2]};
-      R c[3];
-      cross3(axs[j], rel, c);
-      Jm[0][j] = c[0];
-      Jm[1][j] = c[1];
-      Jm[2][j] = c[2];
-      Jm[3][j] = axs[j][2];
-    }
-    const R e4[4] = {pe[0], pe[1], pe[2], ye};
-    R dq[kMaxJ];
-    dls_step<R, 4>(Jm, J, e4, damping, dq);
-    for (int j = 0; j < J; ++j) {
-      R v = q[j] + dq[j];
-      q[j] = v < ch.lo[j] ? ch.lo[j] : (v > ch.hi[j] ? ch.hi[j] : v);
-    }
-  }
-  fk_frames(ch, q, org, axs, ee, Rm);
-  const R pe[3] = {tp[0] - ee[0], tp[1] - ee[1], tp[2] - ee[2]};
-  const R pn = Math<R>::sqrt_((pe[0] * pe[0] + pe[1] * pe[1]) + pe[2] * pe[2]);
-  const R ye = fabs(wrap_yaw(ty - yaw_of(Rm)));
-  *score = pn + ye;
-  return pn < R(kIkPosTol) && ye < R(kIkYawTol);
-}
-
-// _polish_tool_down for one configuration (trajopt.py:726-776): 5-row DLS on position,
-// exact yaw and the tool-z "down" component; full-circle joints wrap; clip.
-template <typename R>
-__device__ bool polish_thread(const ChainDesc<R>& ch, R* q, const R tp[3], R ty) {
-  const int J = ch.J;
-  const R cos_tol = R(0.99998750002604164);  // cos(0.005)
-  const R two_pi = R(6.283185307179586476925286766559);
-  R org[kMaxJ][3], axs[kMaxJ][3], ee[3], Rm[9];
-  for (int it = 0; it < kPolishMaxIters; ++it) {
-    fk_frames(ch, q, org, axs, ee, Rm);
-    const R pe[3] = {tp[0] - ee[0], tp[1] - ee[1], tp[2] - ee[2]};
-    const R ye = wrap_yaw(ty - yaw_of(Rm));
-    const R ax[3] = {Rm[2], Rm[5], Rm[8]};
-    const R pn = Math<R>::sqrt_((pe[0] * pe[0] + pe[1] * pe[1]) + pe[2] * pe[2]);
-    if (pn < R(kIkPosTol) && fabs(ye) < R(kIkYawTol) && -ax[2] > cos_tol) break;
-    R Jm[5][kMaxJ];
-#pragma unroll
-    for (int j = 0; j < kMaxJ; ++j) {
-      if (j >= J) break;
-      const R rel[3] = {ee[0] - org[j][0], ee[1] - org[j][1], ee[2] - org[j][2]};
-      R c[3];
-      cross3(axs[j], rel, c);
-      Jm[0][j] = c[0];
-      Jm[1][j] = c[1];
-      Jm[2][j] = c[2];
-      Jm[3][j] = yaw_jac(Rm, axs[j]);
-      cross3(axs[j], ax, c);
-      Jm[4][j] = c[2];
-    }
-    const R e5[5] = {pe[0], pe[1], pe[2], ye, R(-1) - ax[2]};
-    R dq[kMaxJ];
-    dls_step<R, 5>(Jm, J, e5, R(kIkDamping), dq);
-    for (int j = 0; j < J; ++j) {
-      R v = q[j] + dq[j];
-      if (ch.full_circle[j]) v = ch.lo[j] + np_mod_pos(v - ch.lo[j], two_pi);
-      q[j] = v < ch.lo[j] ? ch.lo[j] : (v > ch.hi[j] ? ch.hi[j] : v);
-    }
-  }
-  fk_frames(ch, q, org, axs, ee, Rm);
-  const R pe[3] = {tp[0] - ee[0], tp[1] - ee[1], tp[2] - ee[2]};
-  const R pn = Math<R>::sqrt_((pe[0] * pe[0] + pe[1] * pe[1]) + pe[2] * pe[2]);
-  return pn < R(kIkPosTol) && fabs(wrap_yaw(ty - yaw_of(Rm))) < R(kIkYawTol) && -Rm[8] > cos_tol;
-}
-
-// Largest arm-sphere penetration (no clamp) against a sphere set (trajopt.py:779-787)
-template <typename R>
-__device__ R arm_worst_pen(const ChainDesc<R>& ch, const R* q, const R (*cen)[3], const R* rad, int n) {
-  R armw[kMaxArmS * 3];
-  R ee[3], Rm[9];
-  fk_eval<R>(ch, q, 1, nullptr, nullptr, armw, 1, ee, Rm);
-  R worst = -INFINITY;
-  for (int s = 0; s < ch.S; ++s)
-    for (int o = 0; o < n; ++o) {
-      const R dx = armw[3 * s] - cen[o][0], dy = armw[3 * s + 1] - cen[o][1], dz = armw[3 * s + 2] - cen[o][2];
-      const R d = Math<R>::sqrt_((dx * dx + dy * dy) + dz * dz);
-      worst = fmax(worst, (ch.arm_r[s] + rad[o]) - d);
-    }
-  return worst;
 }
 
 }  // namespace spasm

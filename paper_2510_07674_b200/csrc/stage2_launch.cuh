@@ -23,7 +23,7 @@ template <typename R>
 inline int al_layout_for(const Traj& tr, int T, AlLayout* L) {
   *L = al_layout<R>(tr.B, T, tr.J, tr.S, tr.SB, tr.NB);
   SPASM_REQUIRE(T >= 2, "segments need at least two waypoints");
-  SPASM_REQUIRE(L->nthreads <= kMaxAlThreads, "too many waypoints per particle (B*T must be <= 288)");
+  SPASM_REQUIRE(L->nthreads <= kMaxAlThreads, "too many waypoints per particle (B*T must be <= 60)");
   SPASM_REQUIRE(L->total <= 227 * 1024, "trajectory particle does not fit in shared memory");
   return SPASM_OK;
 }
@@ -158,8 +158,8 @@ int launch_ik(const Traj& tr, int n_targets, int n_draws, uint64_t seed, uint64_
   if (n_targets <= 0) return SPASM_OK;
   SPASM_REQUIRE(restarts >= 1 && restarts <= 32, "restarts must be in [1, 32]");
   const int64_t groups = (int64_t)n_targets * n_draws;
-  const int bs = 128;
-  const int64_t grid = (groups * 32 + bs - 1) / bs;
+  const int bs = (restarts * kTile + 31) / 32 * 32;
+  const int64_t grid = groups;
   k_ik_group<R><<<(unsigned)grid, bs, 0, s>>>(tr.dev<R>(), n_targets, n_draws, seed, stride, restarts, max_iters,
                                               damping, tpos, tyaw, rows, D, polish, score_statics, out);
   SPASM_CHECK_LAUNCH();
@@ -170,7 +170,7 @@ template <typename R>
 int launch_polish(const Traj& tr, R* Q, const double* tpos, const double* tyaw, int64_t n, uint8_t* ok,
                   cudaStream_t s) {
   if (n <= 0) return SPASM_OK;
-  k_polish<R><<<ceil_div(n, 64), 64, 0, s>>>(tr.dev<R>(), (int)n, Q, tpos, tyaw, ok);
+  k_polish<R><<<ceil_div(n * kTile, 64), 64, 0, s>>>(tr.dev<R>(), (int)n, Q, tpos, tyaw, ok);
   SPASM_CHECK_LAUNCH();
   return SPASM_OK;
 }
