@@ -10,9 +10,11 @@ configs[1] (C2: 3-block stacking with cuboid obstacles, 16k particles, full pipe
     python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c1|c2|c3|c5]
                     [--precision fp32|fp64] [--impl b200|reference]
 
-Multi-GPU (torchrun, one rank per GPU): each rank solves its own seeds (replicas, weak
-scaling, no data-path collective); rank 0 prints one JSON line with whole-job throughput
-over the max-over-ranks time.
+Multi-GPU (torchrun, one rank per GPU): weak scaling. Each restart's particle batch is
+world x the per-GPU (n, m), sharded contiguously across ranks (sharded.solve_sharded: one
+NCCL all-gather of the local elite keys and one of the satisfying candidates per restart,
+no collective inside the step loop; result identical to one GPU solving the whole batch).
+Rank 0 prints one JSON line with whole-job throughput over the max-over-ranks time.
 """
 from __future__ import annotations
 
@@ -212,27 +214,37 @@ def run_b200(args):
     import torch
 
     rank, world, local = dist_env()
+    local = local % max(1, torch.cuda.device_count())
     if world > 1:
         import torch.distributed as dist
 
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl")
+        # nccl on a real multi-GPU node; SPASM_DIST_BACKEND=gloo lets several ranks share one
+        # GPU to exercise the sharded path (tests only; the collectives then stage via host)
+        dist.init_process_group(os.environ.get("SPASM_DIST_BACKEND", "nccl"))
     else:
         torch.cuda.set_device(0)
     from paper_2510_07674_b200.bench_api import _solver_config, effective_max_restarts, solve_scene
     from paper_2510_07674_b200.problems import as_cost_model, load_scene
 
+    from paper_2510_07674_b200.sharded import TorchComm
+
     scene_name, over, stage1_only, desc = WORKLOADS[args.workload]
     scene = load_scene(scene_name)
     model = as_cost_model(scene.problem, precision=args.precision)
+    base = _solver_config(scene, 0, over, False)
+    # weak scaling: every rank keeps the per-GPU batch (n, m); the restart's global batch is
+    # world x (n, m), sharded contiguously (sharded.solve_sharded, NCCL elite exchange)
+    over = {**over, "n": base.n * world, "m": base.m * world}
     cfg = _solver_config(scene, 0, over, False)
     cfg.max_restarts = effective_max_restarts(cfg)
+    comm = TorchComm() if world > 1 else None
 
     def step(seed):
         return solve_scene(scene, seed=seed, solver_overrides=over, no_trajopt=stage1_only, precision=args.precision,
-                           model=model)
+                           model=model, comm=comm)
 
-    seed0 = 1000 * rank
+    seed0 = 0
     for i in range(args.warmup):
         step(seed0 + 100000 + i)
     torch.cuda.synchronize()
@@ -263,12 +275,14 @@ def run_b200(args):
     al_its = sum(s.stats.get("stage2_iterations", 0) for s in sols)
     total_dev, total_wall = sum(dev_ms), sum(wall_ms)
     if world > 1:
-        t = torch.tensor([total_dev, total_wall], device="cuda", dtype=torch.float64)
+        # every rank holds the same (global) result and work count; time = max over ranks
+        red_dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+        t = torch.tensor([total_dev, total_wall], device=red_dev, dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total_dev, total_wall = t.tolist()
-        c = torch.tensor([its, succ, launches], device="cuda", dtype=torch.float64)
+        c = torch.tensor([launches], device=red_dev, dtype=torch.float64)
         dist.all_reduce(c)
-        its, succ, launches = [int(v) for v in c.tolist()]
+        launches = int(c.item())
     clk = clocks.summary()
     sm_mhz = clk["sm_mhz"] or 1965.0
     peak = 2 * 128 * 148 * sm_mhz * 1e6 / 1e12  # FP32 CUDA-core TFLOP/s at the measured SM clock
@@ -284,7 +298,7 @@ def run_b200(args):
                 "traffic": _traffic(f"{args.workload}_{args.precision}_k_solve_al"),
                 "note": "latency-bound: a few dozen CTAs x serial inner steps; see DESIGN.md section 3"}
     else:
-        kern_ms, flops = measure_schedule_kernel(model, cfg)
+        kern_ms, flops = measure_schedule_kernel(model, base)  # one rank's m-row launch
         roof = {"bound": "fp32", "achieved": flops / (kern_ms * 1e-3) / 1e12, "peak": peak, "unit": "TFLOP/s",
                 "kernel": "k_schedule (fused K_lin+K_quad descent)", "kernel_ms": kern_ms, "flops_per_launch": flops,
                 "traffic": _traffic(f"{args.workload}_{args.precision}_k_schedule")}
@@ -312,7 +326,7 @@ def run_b200(args):
         "warmup": args.warmup,
         "ms_per_step": total_dev / args.steps,
         "p50_solve_ms": statistics.median(wall_ms),
-        "success_rate": succ / (args.steps * world),
+        "success_rate": succ / args.steps,
         "higher_is_better": True,
         "scaling": "weak",
         "vs_baseline": None,
@@ -321,7 +335,9 @@ def run_b200(args):
         "config": {"workload": desc, "scene": scene_name, "n": cfg.n, "m": cfg.m, "k_lin": cfg.k_lin,
                    "k_quad": cfg.k_quad, "max_restarts": cfg.max_restarts, "p_return": p_ret,
                    "stage2": not stage1_only, "l2": "flushed (256 MB write) between timed solves",
-                   "parallelism": f"replicas x{world}"},
+                   "parallelism": (f"dp{world}: stage-1 particles sharded across ranks, NCCL all-gather of "
+                                   "elite keys + candidates once per restart; stage 2 on every rank"
+                                   if world > 1 else "single GPU")},
         "e2e": {"value": its / (total_wall * 1e-3), "unit": "particle-iterations/s",
                 "p50_solve_ms": statistics.median(wall_ms), "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                 "api": "bench_api.solve_scene (host scene/config in, host placement/trajectory out)"},

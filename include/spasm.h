@@ -157,6 +157,33 @@ int spasm_solve(const spasm_model* model, int dtype, const spasm_solve_config* c
                 int32_t* trace_ids, void* stream);
 
 
+/* ---- sharded stage-1 restart (multi-GPU, one process per GPU) -------
+ * The two device halves of one restart of particle_opt.solve (particle_opt.py:325-384)
+ * when the restart's N sampled rows are split into contiguous per-rank ranges (the
+ * np.array_split analogue of _BatchOps, particle_opt.py:146-173). The host exchanges
+ * between the halves (NCCL all-gather); results are identical to spasm_solve for any
+ * world size. Workspace: spasm_shard_workspace_bytes(n_local_max, m_local_max).
+ *
+ * spasm_shard_select: sample + LINEAR-evaluate rows [row_lo, row_lo + n_local) of the
+ *   restart's centralized draw (particle_opt.py:326-330), stable-sort them, and write the
+ *   rank's elite run elite[m][2] = {order key, global row} (u64), ascending, padded with
+ *   all-ones records when n_local < m.
+ * spasm_shard_descend: merge the world*m gathered elite records into the global stable
+ *   top-m (select_topk, particle_opt.py:195-200), re-draw the rows at positions
+ *   [pos_lo, pos_hi) of it, run the fused descent schedule (particle_opt.py:266-300,
+ *   359), order the satisfying rows (particle_opt.py:360-365) and re-check the first
+ *   p_return (particle_opt.py:366). candidates (device float64) =
+ *   [n_satisfying, flagged, k, p_return x (position, row, cost, recheck, values[D])]. */
+int64_t spasm_shard_workspace_bytes(const spasm_model* model, int dtype, const spasm_solve_config* cfg,
+                                    int64_t n_local, int64_t m_local);
+int spasm_shard_select(const spasm_model* model, int dtype, const spasm_solve_config* cfg, int restart, int64_t row_lo,
+                       int64_t n_local, const double* warm_dev, int64_t n_warm, void* workspace,
+                       int64_t workspace_bytes, uint64_t* elite, int32_t* launches, void* stream);
+int spasm_shard_descend(const spasm_model* model, int dtype, const spasm_solve_config* cfg, int restart,
+                        const uint64_t* elite_all, int world, int64_t pos_lo, int64_t pos_hi, const double* warm_dev,
+                        int64_t n_warm, void* workspace, int64_t workspace_bytes, double* candidates,
+                        int32_t* launches, void* stream);
+
 /* =====================================================================================
  * Stage 2: trajectory optimization (reference trajopt.py / robot.py)
  * ===================================================================================== */

@@ -181,6 +181,17 @@ SIGNATURES = {
         [c_void_p, c_int, POINTER(spasm_solve_config), c_void_p, c_int64, c_void_p, c_int64, c_void_p, c_void_p,
          c_void_p, POINTER(spasm_solve_report), c_void_p, c_void_p, c_void_p, c_void_p],
     ),
+    "spasm_shard_workspace_bytes": (c_int64, [c_void_p, c_int, POINTER(spasm_solve_config), c_int64, c_int64]),
+    "spasm_shard_select": (
+        c_int,
+        [c_void_p, c_int, POINTER(spasm_solve_config), c_int, c_int64, c_int64, c_void_p, c_int64, c_void_p, c_int64,
+         c_void_p, c_void_p, c_void_p],
+    ),
+    "spasm_shard_descend": (
+        c_int,
+        [c_void_p, c_int, POINTER(spasm_solve_config), c_int, c_void_p, c_int, c_int64, c_int64, c_void_p, c_int64,
+         c_void_p, c_int64, c_void_p, c_void_p, c_void_p],
+    ),
     "spasm_traj_create": (c_int, [POINTER(c_void_p), POINTER(spasm_chain), POINTER(spasm_traj_desc)]),
     "spasm_traj_destroy": (None, [c_void_p]),
     "spasm_traj_segments": (c_int, [c_void_p]),

@@ -55,8 +55,12 @@ class SceneSolution:
 
 def solve_scene(scene: Scene, *, seed: int = 0, threads: int = 1, solver_overrides: Optional[dict] = None,
                 trajopt_overrides: Optional[dict] = None, quadratic_only: bool = False, no_trajopt: bool = False,
-                warm_seeds=None, precision: str = "fp32", model=None) -> SceneSolution:
-    """Run the pipeline once; failures are normal returns (bench.py:168-268)."""
+                warm_seeds=None, precision: str = "fp32", model=None, comm=None) -> SceneSolution:
+    """Run the pipeline once; failures are normal returns (bench.py:168-268).
+
+    ``comm`` (a ``sharded.TorchComm`` over >1 ranks) shards stage 1's particles across the
+    ranks (``sharded.solve_sharded``; identical result); stage 2 then runs on every rank
+    from the identical stage-1 result."""
     if isinstance(scene.problem, MotionProblem):
         if no_trajopt:
             raise ValueError("point-to-point scenes have no placement stage")
@@ -68,7 +72,12 @@ def solve_scene(scene: Scene, *, seed: int = 0, threads: int = 1, solver_overrid
     config = replace(config, max_restarts=effective_max_restarts(config))
     run_stage2 = scene.chain is not None and not no_trajopt
     t0 = time.perf_counter()
-    result = solve(model, config, warm_seeds=warm_seeds, threads=threads)
+    if comm is not None and comm.world > 1:
+        from .sharded import solve_sharded
+
+        result = solve_sharded(model, config, comm=comm, warm_seeds=warm_seeds)
+    else:
+        result = solve(model, config, warm_seeds=warm_seeds, threads=threads)
     restarts_run = result.report.restarts + 1 if result.success else config.max_restarts
     stats = {"stage1_iterations": restarts_run * config.m * (config.k_lin + config.k_quad),
              "stage1_evaluations": restarts_run * config.n, "stage1_launches": result.report.launches,

@@ -14,6 +14,7 @@
 #include "model.hpp"
 #include "rng.cuh"
 #include "scene.cuh"
+#include "launchers.hpp"
 
 namespace spasm {
 
@@ -21,43 +22,6 @@ static thread_local std::string g_last_error;
 void set_last_error(const std::string& msg) { g_last_error = msg; }
 const char* last_error() { return g_last_error.c_str(); }
 
-void seedseq_pcg64(uint64_t seed, const uint64_t* spawn_key, int n_spawn, uint64_t out[4]);
-
-// ---- launchers (explicitly instantiated in stage1_f32.cu / stage1_f64.cu) ----------
-template <typename R> int launch_evaluate(const Model&, const R*, int64_t, int, R*, cudaStream_t);
-template <typename R> int launch_gradient(const Model&, const R*, int64_t, int, R*, cudaStream_t);
-template <typename R>
-int launch_sample_eval(const Model&, const Pcg64State&, int64_t, int64_t, const double*, int64_t, int, uint64_t,
-                       uint32_t, R*, typename KeyOf<R>::type*, uint32_t*, cudaStream_t);
-template <typename R>
-int launch_schedule(const Model&, const R*, const uint32_t*, int64_t, int, int, double, double, double, R*, R*,
-                    uint8_t*, unsigned int*, R*, uint8_t*, int, cudaStream_t);
-template <typename R>
-int launch_sample(const Bounds64&, int, const Pcg64State&, int64_t, int64_t, const double*, int64_t, int, uint64_t,
-                  uint32_t, R*, cudaStream_t);
-template <typename R>
-int launch_step(R*, const R*, int64_t, int, R, const R*, const R*, uint8_t*, cudaStream_t);
-template <typename R>
-int launch_sort(typename KeyOf<R>::type*, uint32_t*, typename KeyOf<R>::type*, uint32_t*, int64_t, unsigned int*,
-                bool*, cudaStream_t);
-template <typename R>
-int launch_sat_keys(const R*, int64_t, double, typename KeyOf<R>::type*, uint32_t*, unsigned int*, cudaStream_t);
-
-extern template int launch_evaluate<float>(const Model&, const float*, int64_t, int, float*, cudaStream_t);
-extern template int launch_evaluate<double>(const Model&, const double*, int64_t, int, double*, cudaStream_t);
-
-static Pcg64State restart_state(uint64_t seed, uint64_t restart) {
-  uint64_t o[4];
-  seedseq_pcg64(seed, &restart, 1, o);
-  Pcg64State s;
-  s.state_hi = o[0];
-  s.state_lo = o[1];
-  s.inc_hi = o[2];
-  s.inc_lo = o[3];
-  return s;
-}
-
-static inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
 // ---- small helper kernels for the solve loop --------------------------------------
 template <typename R>
@@ -460,19 +424,6 @@ void spasm_model_destroy(spasm_model* model) {
 
 int spasm_model_dimension(const spasm_model* model) { return model ? model->dim : -1; }
 
-#define SPASM_DTYPE_SWITCH(dtype, ...)                          \
-  do {                                                          \
-    if ((dtype) == SPASM_F32) {                                 \
-      using R = float;                                          \
-      __VA_ARGS__                                               \
-    } else if ((dtype) == SPASM_F64) {                          \
-      using R = double;                                         \
-      __VA_ARGS__                                               \
-    } else {                                                    \
-      spasm::set_last_error("dtype must be SPASM_F32 or SPASM_F64"); \
-      return SPASM_ERR_USAGE;                                   \
-    }                                                           \
-  } while (0)
 
 int spasm_evaluate(const spasm_model* model, int dtype, const void* values, int64_t P, int mode, void* costs,
                    void* stream) {
@@ -507,7 +458,7 @@ int spasm_sample(int dtype, int D, const double* lower, const double* upper, uin
     b.hi[d] = upper[d];
   }
   const Pcg64State st = restart_state(seed, restart);
-  SPASM_DTYPE_SWITCH(dtype, return launch_sample<R>(b, D, st, row_offset, N, warm_dev, n_warm, sampler, seed,
+  SPASM_DTYPE_SWITCH(dtype, return launch_sample<R>(b, D, st, row_offset, nullptr, N, warm_dev, n_warm, sampler, seed,
                                                     (uint32_t)restart, static_cast<R*>(values), as_stream(stream)););
 }
 

@@ -143,15 +143,20 @@ __global__ void k_sample_eval(const typename E::Scene sc, const Bounds64 bd, Pcg
   idx[p] = (uint32_t)(row_offset + p);
 }
 
+// rows (optional): draw the listed global rows instead of [row_offset, row_offset+N), so a
+// rank can re-create any row of the centralized draw (the sharded top-M, shard.cu).
 template <typename R>
-__global__ void k_sample(const Bounds64 bd, Pcg64State st, int64_t row_offset, int64_t N, int D,
-                         const double* __restrict__ warm, int64_t n_warm, int use_philox, uint64_t philox_seed,
-                         uint32_t restart, R* __restrict__ values) {
+__global__ void k_sample(const Bounds64 bd, Pcg64State st, int64_t row_offset, const uint32_t* __restrict__ rows,
+                         int64_t N, int D, const double* __restrict__ warm, int64_t n_warm, int use_philox,
+                         uint64_t philox_seed, uint32_t restart, R* __restrict__ values) {
   const int bs = blockDim.x;
   R* base = particle_smem<R>(0);
   const int64_t p0 = (int64_t)blockIdx.x * bs;
   const int64_t p = p0 + threadIdx.x;
-  if (p < N) sample_row<R>(base + threadIdx.x, bs, st, row_offset + p, D, bd, warm, n_warm, use_philox, philox_seed, restart);
+  if (p < N) {
+    const int64_t grow = rows ? (int64_t)rows[p] : row_offset + p;
+    sample_row<R>(base + threadIdx.x, bs, st, grow, D, bd, warm, n_warm, use_philox, philox_seed, restart);
+  }
   __syncthreads();
   store_rows<R>(values, base, p0, N, D, bs);
 }

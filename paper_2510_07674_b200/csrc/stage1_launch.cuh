@@ -130,14 +130,15 @@ int launch_schedule(const Model& m, const R* src, const uint32_t* rows, int64_t 
 }
 
 template <typename R>
-int launch_sample(const Bounds64& bd, int D, const Pcg64State& st, int64_t row_offset, int64_t N, const double* warm,
-                  int64_t n_warm, int use_philox, uint64_t seed, uint32_t restart, R* values, cudaStream_t s) {
+int launch_sample(const Bounds64& bd, int D, const Pcg64State& st, int64_t row_offset, const uint32_t* rows, int64_t N,
+                  const double* warm, int64_t n_warm, int use_philox, uint64_t seed, uint32_t restart, R* values,
+                  cudaStream_t s) {
   if (N <= 0) return SPASM_OK;
   const size_t per = (size_t)D * sizeof(R);
   const int bs = pick_block(N, per);
   allow_big_smem(k_sample<R>);
-  k_sample<R><<<ceil_div(N, bs), bs, per * bs, s>>>(bd, st, row_offset, N, D, warm, n_warm, use_philox, seed, restart,
-                                                    values);
+  k_sample<R><<<ceil_div(N, bs), bs, per * bs, s>>>(bd, st, row_offset, rows, N, D, warm, n_warm, use_philox, seed,
+                                                    restart, values);
   SPASM_CHECK_LAUNCH();
   return SPASM_OK;
 }

@@ -1,0 +1,114 @@
+"""Multi-rank stage 1 on CPU: world_size 2 and 3 gloo groups drive
+``sharded.solve_sharded`` with oracle-backed device halves, and must reproduce the
+single-process reference solve (oracle/stage1.solve, pinned to the reference goldens)
+exactly: success, restarts, indices, particles and costs. Also covers the host pieces
+(row partitioning, candidate merge) directly."""
+from __future__ import annotations
+
+import os
+import tempfile
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from conftest import ROOT
+from oracle import stage1 as orc
+from paper_2510_07674_b200.particle_opt import OptimizerConfig
+from paper_2510_07674_b200.problems import load_scene
+from paper_2510_07674_b200.sharded import TorchComm, merge_candidates, shard_range, solve_sharded
+
+
+@pytest.mark.parametrize("n,world", [(10, 3), (7, 2), (2, 4), (1 << 16, 8), (5, 1)])
+def test_shard_range_is_array_split(n, world):
+    parts = np.array_split(np.arange(n), world)
+    for r in range(world):
+        lo, hi = shard_range(n, world, r)
+        assert list(range(lo, hi)) == parts[r].tolist()
+
+
+def test_merge_candidates_orders_by_cost_then_position_and_rechecks():
+    D, p, eps = 2, 3, 1e-3
+
+    def block(n_sat, flagged, recs):
+        b = np.zeros(3 + p * (4 + D))
+        b[0], b[1], b[2] = n_sat, flagged, len(recs)
+        for c, r in enumerate(recs):
+            b[3 + c * (4 + D): 3 + (c + 1) * (4 + D)] = r
+        return b
+
+    # (pos, row, cost, recheck, v0, v1)
+    r0 = [(1, 11, 1e-4, 1e-4, 0, 0), (4, 14, 3e-4, 3e-4, 0, 0)]
+    r1 = [(2, 22, 1e-4, 2e-3, 1, 1), (0, 20, 2e-4, 2e-4, 1, 1), (3, 23, 5e-4, 5e-4, 1, 1)]
+    n_sat, fl, chosen = merge_candidates(np.stack([block(2, 1, r0), block(5, 2, r1)]), D, p, eps)
+    assert (n_sat, fl) == (7, 3)
+    # stable order: (1e-4, pos 1), (1e-4, pos 2) [fails re-check], (2e-4, pos 0)
+    assert chosen[:, 1].tolist() == [11, 20]
+
+
+def _worker(rank, world, init_file, case, out_path):
+    dist.init_process_group("gloo", init_method=f"file://{init_file}", rank=rank, world_size=world)
+    try:
+        from shard_oracle_ops import OracleShardOps
+
+        scene = load_scene(case["scene"])
+        o = orc.oracle_model(scene.problem)
+        kw = {**scene.solver_overrides, **case["over"]}
+        ocfg = orc.OracleConfig(**kw)
+        cfg = OptimizerConfig(**kw)
+        warm = case.get("warm")
+        ops = OracleShardOps(o, ocfg, warm)
+        res = solve_sharded(o, cfg, comm=TorchComm(), ops=ops, warm_seeds=warm)
+        if rank == 0:
+            np.savez(out_path, success=res.success, restarts=res.report.restarts, indices=res.indices,
+                     particles=res.particles, costs=res.costs, n_sat=res.report.n_satisfying,
+                     flagged=res.report.flagged, steps=res.report.steps)
+    finally:
+        dist.destroy_process_group()
+
+
+def _run_world(world, case):
+    import sys
+
+    tests_dir = os.path.join(ROOT, "tests")
+    if tests_dir not in sys.path:
+        sys.path.insert(0, tests_dir)
+    with tempfile.TemporaryDirectory() as d:
+        out = os.path.join(d, "res.npz")
+        mp.spawn(_worker, args=(world, os.path.join(d, "store"), case, out), nprocs=world, join=True)
+        return dict(np.load(out))
+
+
+CASES = [
+    # tetris5 restarts: a few failing restarts before success exercise the loop
+    {"scene": "tetris5", "over": {"n": 600, "m": 96, "seed": 3, "max_restarts": 6}},
+    # n_local < m on every rank (padded elite runs), odd split
+    {"scene": "tower4", "over": {"n": 150, "m": 120, "seed": 1, "max_restarts": 3, "k_lin": 8, "k_quad": 8}},
+    # warm start rows live on rank 0 only
+    {"scene": "tetris5", "over": {"n": 400, "m": 64, "seed": 7, "max_restarts": 2}},
+]
+
+
+@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("ci", range(len(CASES)))
+def test_sharded_solve_matches_single_process_reference(world, ci):
+    case = dict(CASES[ci])
+    scene = load_scene(case["scene"])
+    o = orc.oracle_model(scene.problem)
+    kw = {**scene.solver_overrides, **case["over"]}
+    if ci == 2:
+        ref0 = orc.solve(o, orc.OracleConfig(**{**kw, "seed": 11, "max_restarts": 4}))
+        assert ref0.success
+        case["warm"] = ref0.particles[:2]
+    ref = orc.solve(o, orc.OracleConfig(**kw), warm_seeds=case.get("warm"))
+    got = _run_world(world, case)
+    assert bool(got["success"]) == ref.success
+    assert int(got["restarts"]) == ref.restarts
+    assert int(got["n_sat"]) == ref.n_satisfying
+    assert int(got["flagged"]) == ref.flagged
+    assert int(got["steps"]) == ref.steps
+    np.testing.assert_array_equal(got["indices"], ref.indices)
+    np.testing.assert_array_equal(got["particles"], ref.particles)
+    np.testing.assert_array_equal(got["costs"], ref.costs)
