@@ -138,6 +138,7 @@ class spasm_al_result(ctypes.Structure):
 SIGNATURES = {
     "spasm_last_error": (c_char_p, []),
     "spasm_version": (c_int, []),
+    "spasm_set_option": (c_int, [c_char_p, c_int]),
     "spasm_tetris_model_create": (
         c_int,
         [POINTER(c_void_p), c_int, c_void_p, c_void_p, c_void_p, c_int, c_void_p, c_void_p, c_void_p,
@@ -249,6 +250,9 @@ def load() -> ctypes.CDLL:
         fn.restype = res
         fn.argtypes = args
     _lib = lib
+    tile = os.environ.get("SPASM_STAGE1_TILE")  # tuning/profiling switch, see spasm_set_option
+    if tile is not None:
+        check(lib.spasm_set_option(b"stage1_tile", int(tile)), "SPASM_STAGE1_TILE")
     return lib
 
 

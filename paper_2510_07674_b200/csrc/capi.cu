@@ -22,6 +22,9 @@ static thread_local std::string g_last_error;
 void set_last_error(const std::string& msg) { g_last_error = msg; }
 const char* last_error() { return g_last_error.c_str(); }
 
+static int g_stage1_tile = -1;  // spasm_set_option("stage1_tile", ...)
+int stage1_tile_mode() { return g_stage1_tile; }
+
 
 // ---- small helper kernels for the solve loop --------------------------------------
 template <typename R>
@@ -323,7 +326,86 @@ static void fill_tetris(TetrisScene<R>& s, int n_bodies, const int32_t* spb, con
   }
 }
 
+// The fp32 tile kernel covers tetris scenes with 4 spheres per body of one radius, the 4
+// box walls, fixed yaw and at most kTileMaxBodies bodies (stage1_tile.cuh).
+static void fill_tile(Model& m, int n_bodies, const int32_t* spb, const double* lc, const double* rad, int n_static,
+                      const double* sc, const double* sr, const double* sn, double wbb, double wbs, double wh,
+                      double zs, int free_yaw) {
+  m.tile_ok = false;
+  if (free_yaw || n_bodies < 1 || n_bodies > kTileMaxBodies || n_static != kTileWalls) return;
+  for (int i = 0; i < n_bodies; ++i)
+    if (spb[i] != kTileSpb) return;
+  const int S = n_bodies * kTileSpb;
+  for (int a = 1; a < S; ++a)
+    if (rad[a] != rad[0]) return;
+  TetrisTileScene& t = m.tile;
+  std::memset(&t, 0, sizeof(t));
+  auto dup = [](float v) { return make_float2(v, v); };
+  t.n = n_bodies;
+  for (int a = 0; a < S; ++a) {
+    t.lx[a] = (float)lc[3 * a];
+    t.ly[a] = (float)lc[3 * a + 1];
+    t.lz[a] = (float)lc[3 * a + 2];
+    t.lx2[a] = dup(t.lx[a]);
+    t.ly2[a] = dup(t.ly[a]);
+    t.lz2[a] = dup(t.lz[a]);
+  }
+  for (int w = 0; w < kTileWalls; ++w) {
+    const double R = sr[w];
+    t.ax[w] = (float)(sc[3 * w] + R * sn[3 * w]);
+    t.ay[w] = (float)(sc[3 * w + 1] + R * sn[3 * w + 1]);
+    t.az[w] = (float)(sc[3 * w + 2] + R * sn[3 * w + 2]);
+    t.nx[w] = (float)sn[3 * w];
+    t.ny[w] = (float)sn[3 * w + 1];
+    t.nz[w] = (float)sn[3 * w + 2];
+    t.wr[w] = (float)R;
+    t.wrn_x[w] = (float)R * t.nx[w];
+    t.wrn_y[w] = (float)R * t.ny[w];
+    t.wrn_z[w] = (float)R * t.nz[w];
+    t.wr2[w] = (float)R * (float)R;
+    t.two_wr[w] = 2.f * (float)R;
+    t.ax2[w] = dup(t.ax[w]);
+    t.ay2[w] = dup(t.ay[w]);
+    t.az2[w] = dup(t.az[w]);
+    t.nx2[w] = dup(t.nx[w]);
+    t.ny2[w] = dup(t.ny[w]);
+    t.nz2[w] = dup(t.nz[w]);
+    t.wr_2[w] = dup(t.wr[w]);
+    t.wrnx2[w] = dup(t.wrn_x[w]);
+    t.wrny2[w] = dup(t.wrn_y[w]);
+    t.wrnz2[w] = dup(t.wrn_z[w]);
+    t.wrsq2[w] = dup(t.wr2[w]);
+    t.twr2[w] = dup(t.two_wr[w]);
+  }
+  t.r = (float)rad[0];
+  t.rs = 2.f * t.r;
+  t.rs2 = t.rs * t.rs;
+  t.r_2 = dup(t.r);
+  t.rs_2 = dup(t.rs);
+  t.rs2_2 = dup(t.rs2);
+  t.w_bb = (float)wbb;
+  t.w_bs = (float)wbs;
+  t.w_h = (float)wh;
+  t.z_star = (float)zs;
+  for (int d = 0; d < 3 * n_bodies; ++d) {
+    t.lower[d] = (float)m.bounds.lo[d];
+    t.upper[d] = (float)m.bounds.hi[d];
+  }
+  m.tile_ok = true;
+}
+
 extern "C" {
+
+int spasm_set_option(const char* key, int value) {
+  SPASM_REQUIRE(key != nullptr, "null option key");
+  if (std::strcmp(key, "stage1_tile") == 0) {
+    SPASM_REQUIRE(value >= -1 && value <= 4, "stage1_tile must be -1 (auto), 0 (off) or 1..4");
+    g_stage1_tile = value;
+    return SPASM_OK;
+  }
+  set_last_error(std::string("unknown option: ") + key);
+  return SPASM_ERR_USAGE;
+}
 
 int spasm_tetris_model_create(spasm_model** out, int n_bodies, const int32_t* spheres_per_body,
                               const double* local_centers, const double* radii, int n_static,
@@ -355,6 +437,8 @@ int spasm_tetris_model_create(spasm_model** out, int n_bodies, const int32_t* sp
   fill_tetris<double>(m->td, n_bodies, spheres_per_body, local_centers, radii, n_static, static_centers,
                       static_radii, static_normals, w_block_block, w_block_wall, w_height, z_star, free_yaw,
                       m->bounds, D);
+  fill_tile(*m, n_bodies, spheres_per_body, local_centers, radii, n_static, static_centers, static_radii,
+            static_normals, w_block_block, w_block_wall, w_height, z_star, free_yaw);
   *out = m;
   return SPASM_OK;
 }

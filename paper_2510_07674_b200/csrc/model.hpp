@@ -13,6 +13,9 @@ struct Model {
   TetrisScene<double> td;
   TowerScene<float> wf;
   TowerScene<double> wd;
+  // fp32 tile-kernel scene, valid when tile_ok (stage1_tile.cuh)
+  TetrisTileScene tile;
+  bool tile_ok = false;
   // double-precision bounds for the bit-exact sampler (numpy draws in float64)
   Bounds64 bounds;
   // pinned staging for solve results (grown on demand, never inside a kernel sequence)

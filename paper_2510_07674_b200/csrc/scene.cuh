@@ -58,4 +58,26 @@ struct TowerScene {
   R lower[kMaxDim], upper[kMaxDim];
 };
 
+// fp32 tile-kernel scene (stage1_tile.cuh): the tetris scenes with 4 spheres per body of
+// one radius, 4 wall spheres, fixed yaw and at most 8 bodies.
+constexpr int kTileMaxBodies = 8;
+constexpr int kTileSpb = 4;
+constexpr int kTileWalls = 4;
+
+// Host-built compact scene for the tile kernel (scalar + duplicated-pair copies of every
+// constant the pair loops read, so packed ops take them as uniform-register operands).
+struct TetrisTileScene {
+  int n;
+  float lx[kTileMaxBodies * kTileSpb], ly[kTileMaxBodies * kTileSpb], lz[kTileMaxBodies * kTileSpb];
+  float2 lx2[kTileMaxBodies * kTileSpb], ly2[kTileMaxBodies * kTileSpb], lz2[kTileMaxBodies * kTileSpb];
+  float ax[kTileWalls], ay[kTileWalls], az[kTileWalls], nx[kTileWalls], ny[kTileWalls], nz[kTileWalls],
+      wr[kTileWalls], wrn_x[kTileWalls], wrn_y[kTileWalls], wrn_z[kTileWalls], wr2[kTileWalls], two_wr[kTileWalls];
+  float2 ax2[kTileWalls], ay2[kTileWalls], az2[kTileWalls], nx2[kTileWalls], ny2[kTileWalls], nz2[kTileWalls],
+      wr_2[kTileWalls], wrnx2[kTileWalls], wrny2[kTileWalls], wrnz2[kTileWalls], wrsq2[kTileWalls], twr2[kTileWalls];
+  float r, rs, rs2;  // uniform sphere radius, rsum = 2r, rsum^2
+  float2 r_2, rs_2, rs2_2;
+  float w_bb, w_bs, w_h, z_star;
+  float lower[kTileMaxBodies * 3], upper[kTileMaxBodies * 3];
+};
+
 }  // namespace spasm

@@ -2,11 +2,20 @@
 // per precision (stage1_f32.cu / stage1_f64.cu) so each precision gets its own
 // compiler flags (fp64 is built with -fmad=false to keep numpy's rounding per op).
 #pragma once
+#include <type_traits>
 #include "model.hpp"
 #include "sort.cuh"
 #include "stage1_kernels.cuh"
 
 namespace spasm {
+
+// Stage-1 tile-kernel switch (spasm_set_option("stage1_tile", v)): -1 auto, 0 generic
+// kernel only, 1..4 force a tile variant (stage1tile_f32.cu).
+int stage1_tile_mode();
+// fp32 tetris tile schedule (stage1tile_f32.cu); returns -1 when not applicable.
+int launch_schedule_tile(const Model& m, const float* src, const uint32_t* rows, int64_t M, int k_lin, int k_quad,
+                         double eta, double alpha, float* out_values, float* out_cost, uint8_t* flagged,
+                         unsigned int* flagged_count, cudaStream_t s);
 
 inline int pick_block(int64_t P, size_t per_thread_bytes) {
   int bs = 128;
@@ -108,6 +117,13 @@ int launch_schedule(const Model& m, const R* src, const uint32_t* rows, int64_t 
                     double eta, double alpha, double eps, R* out_values, R* out_cost, uint8_t* flagged,
                     unsigned int* flagged_count, R* trace_cost, uint8_t* trace_sat, int n_traced, cudaStream_t s) {
   if (M <= 0) return SPASM_OK;
+  if constexpr (std::is_same<R, float>::value) {
+    if (trace_cost == nullptr) {
+      const int r = launch_schedule_tile(m, src, rows, M, k_lin, k_quad, eta, alpha, out_values, out_cost, flagged,
+                                         flagged_count, s);
+      if (r != -1) return r;
+    }
+  }
   return dispatch_model<R>(m, [&](auto e, const auto& sc) -> int {
     using E = decltype(e);
     const size_t per = (size_t)(2 * sc.dim + E::scratch_per_thread(sc)) * sizeof(R);
