@@ -338,51 +338,57 @@ static void fill_tile(Model& m, int n_bodies, const int32_t* spb, const double* 
   const int S = n_bodies * kTileSpb;
   for (int a = 1; a < S; ++a)
     if (rad[a] != rad[0]) return;
+  // walls must be box_wall_spheres' layout: normals +x, -x, +y, -y, one radius, one plane
+  static const double kN[kTileWalls][3] = {{1, 0, 0}, {-1, 0, 0}, {0, 1, 0}, {0, -1, 0}};
+  for (int w = 0; w < kTileWalls; ++w) {
+    for (int k = 0; k < 3; ++k)
+      if (sn[3 * w + k] != kN[w][k]) return;
+    if (sr[w] != sr[0] || sc[3 * w + 2] != sc[2]) return;
+  }
+  if (sc[1] != sc[4] || sc[6] != sc[9]) return;
   TetrisTileScene& t = m.tile;
   std::memset(&t, 0, sizeof(t));
-  auto dup = [](float v) { return make_float2(v, v); };
   t.n = n_bodies;
   for (int a = 0; a < S; ++a) {
     t.lx[a] = (float)lc[3 * a];
     t.ly[a] = (float)lc[3 * a + 1];
     t.lz[a] = (float)lc[3 * a + 2];
-    t.lx2[a] = dup(t.lx[a]);
-    t.ly2[a] = dup(t.ly[a]);
-    t.lz2[a] = dup(t.lz[a]);
   }
+  auto pack = [](float lo, float hi) {
+    uint32_t l, h;
+    std::memcpy(&l, &lo, 4);
+    std::memcpy(&h, &hi, 4);
+    return (unsigned long long)l | ((unsigned long long)h << 32);
+  };
+  for (int a = 0; a < S; a += 2) {
+    t.px[a / 2] = pack(t.lx[a], t.lx[a + 1]);
+    t.py[a / 2] = pack(t.ly[a], t.ly[a + 1]);
+    t.pz[a / 2] = pack(t.lz[a], t.lz[a + 1]);
+  }
+  const double R = sr[0];
   for (int w = 0; w < kTileWalls; ++w) {
-    const double R = sr[w];
-    t.ax[w] = (float)(sc[3 * w] + R * sn[3 * w]);
-    t.ay[w] = (float)(sc[3 * w + 1] + R * sn[3 * w + 1]);
-    t.az[w] = (float)(sc[3 * w + 2] + R * sn[3 * w + 2]);
-    t.nx[w] = (float)sn[3 * w];
-    t.ny[w] = (float)sn[3 * w + 1];
-    t.nz[w] = (float)sn[3 * w + 2];
-    t.wr[w] = (float)R;
-    t.wrn_x[w] = (float)R * t.nx[w];
-    t.wrn_y[w] = (float)R * t.ny[w];
-    t.wrn_z[w] = (float)R * t.nz[w];
-    t.wr2[w] = (float)R * (float)R;
-    t.two_wr[w] = 2.f * (float)R;
-    t.ax2[w] = dup(t.ax[w]);
-    t.ay2[w] = dup(t.ay[w]);
-    t.az2[w] = dup(t.az[w]);
-    t.nx2[w] = dup(t.nx[w]);
-    t.ny2[w] = dup(t.ny[w]);
-    t.nz2[w] = dup(t.nz[w]);
-    t.wr_2[w] = dup(t.wr[w]);
-    t.wrnx2[w] = dup(t.wrn_x[w]);
-    t.wrny2[w] = dup(t.wrn_y[w]);
-    t.wrnz2[w] = dup(t.wrn_z[w]);
-    t.wrsq2[w] = dup(t.wr2[w]);
-    t.twr2[w] = dup(t.two_wr[w]);
+    const int axis = w < 2 ? 0 : 1;
+    t.wall_a[w] = (float)(sc[3 * w + axis] + R * sn[3 * w + axis]);  // tangent point
   }
+  t.wall_ay_x = (float)sc[1];
+  t.wall_ax_y = (float)sc[6];
+  t.wall_az = (float)sc[2];
+  t.wr = (float)R;
+  t.wr2 = (float)R * (float)R;
+  t.two_wr = 2.f * (float)R;
   t.r = (float)rad[0];
+  t.wa_x = pack(t.wall_a[0], t.wall_a[1]);
+  t.wa_y = pack(t.wall_a[2], t.wall_a[3]);
+  t.two_wr_pm = pack(t.two_wr, -t.two_wr);
+  t.wr_pm = pack(t.wr, -t.wr);
+  t.wr2_d = pack(t.wr2, t.wr2);
+  t.wr_d = pack(t.wr, t.wr);
+  t.r_d = pack(t.r, t.r);
   t.rs = 2.f * t.r;
   t.rs2 = t.rs * t.rs;
-  t.r_2 = dup(t.r);
-  t.rs_2 = dup(t.rs);
-  t.rs2_2 = dup(t.rs2);
+  t.rs_d = pack(t.rs, t.rs);
+  t.m1_d = pack(-1.f, -1.f);
+  t.tiny_d = pack(1e-30f, 1e-30f);
   t.w_bb = (float)wbb;
   t.w_bs = (float)wbs;
   t.w_h = (float)wh;

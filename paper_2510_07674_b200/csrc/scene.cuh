@@ -69,13 +69,18 @@ constexpr int kTileWalls = 4;
 struct TetrisTileScene {
   int n;
   float lx[kTileMaxBodies * kTileSpb], ly[kTileMaxBodies * kTileSpb], lz[kTileMaxBodies * kTileSpb];
-  float2 lx2[kTileMaxBodies * kTileSpb], ly2[kTileMaxBodies * kTileSpb], lz2[kTileMaxBodies * kTileSpb];
-  float ax[kTileWalls], ay[kTileWalls], az[kTileWalls], nx[kTileWalls], ny[kTileWalls], nz[kTileWalls],
-      wr[kTileWalls], wrn_x[kTileWalls], wrn_y[kTileWalls], wrn_z[kTileWalls], wr2[kTileWalls], two_wr[kTileWalls];
-  float2 ax2[kTileWalls], ay2[kTileWalls], az2[kTileWalls], nx2[kTileWalls], ny2[kTileWalls], nz2[kTileWalls],
-      wr_2[kTileWalls], wrnx2[kTileWalls], wrny2[kTileWalls], wrnz2[kTileWalls], wrsq2[kTileWalls], twr2[kTileWalls];
+  // the same offsets as packed pairs (spheres 2k, 2k+1 of the table) for f32x2 operands
+  unsigned long long px[kTileMaxBodies * kTileSpb / 2], py[kTileMaxBodies * kTileSpb / 2],
+      pz[kTileMaxBodies * kTileSpb / 2];
+  // walls in box_wall_spheres order (+x, -x, +y, -y inward normals): tangent-point
+  // coordinate along each wall's axis, the shared off-axis tangent coordinates, radius R
+  float wall_a[kTileWalls], wall_ay_x, wall_ax_y, wall_az;
+  float wr, wr2, two_wr;
+  // packed wall constants (x walls, y walls as f32x2 pairs): tangent coordinates (a0, a1),
+  // (a2, a3); (2R, -2R); (R, -R); and duplicated R^2, R, r
+  unsigned long long wa_x, wa_y, two_wr_pm, wr_pm, wr2_d, wr_d, r_d;
+  unsigned long long rs_d, m1_d, tiny_d;  // duplicated rsum, -1, 1e-30
   float r, rs, rs2;  // uniform sphere radius, rsum = 2r, rsum^2
-  float2 r_2, rs_2, rs2_2;
   float w_bb, w_bs, w_h, z_star;
   float lower[kTileMaxBodies * 3], upper[kTileMaxBodies * 3];
 };

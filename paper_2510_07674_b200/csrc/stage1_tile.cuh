@@ -1,159 +1,248 @@
-// fp32 stage-1 descent kernel specialised for the tetris packing scenes (the C3/C5 hot
+// fp32 stage-1 descent kernel specialised for the tetris packing scenes (the C1/C3/C5 hot
 // loop): k_schedule_tile runs the whole K_lin + K_quad schedule (particle_opt.py:266-300)
 // plus the final QUADRATIC cost with every table index known at compile time.
 //
 // Differences from the generic k_schedule (stage1_kernels.cuh), same semantics:
 //   * the body count N is a template parameter, every pair loop is fully unrolled, the
 //     particle state x and gradient g live in registers and every scene constant is a
-//     constant-bank / uniform-register operand (no address arithmetic in the pair loop);
-//   * V is the per-lane arithmetic type (float). Packing two particles per thread into
-//     sm_100a FFMA2/FADD2 was tried and dropped: cicc -O3 needs > 15 min per unrolled
-//     instantiation and ptxas then uses ~250 registers;
-//   * LA > 1 splits one particle's a-spheres across LA lanes of a warp for small M;
-//     partial gradients are combined with a butterfly __shfl_xor (north_star: warp-shuffle
-//     reductions over spheres), the height term is added after the reduction, and every
-//     lane applies the identical clamped step.
-//   * pair math (fixed yaw, uniform sphere radius r, rsum = 2r):
-//       linear:    s = [d2 < rsum^2] / d            (d2 = 0 -> zero gradient, the
-//       quadratic: s = max(rsum / d - 1, 0) = pen/d  reference's coincident-centre rule)
-//     with 1/d = rsqrt(max(d2, 1e-30)), d cost/d ca = -w s (ca - cb) (x2 in quadratic).
-// Wall pairs use the cancellation-free form of pen_static_acc (stage1_models.cuh).
+//     constant-bank operand (no address arithmetic in the pair loops);
+//   * LA lanes of a warp share one particle: lane l owns a-sphere l*SA..l*SA+SA-1 of every
+//     body (vs all spheres of the later bodies and the walls). Partial gradients are
+//     combined with a butterfly __shfl_xor (north_star: warp-shuffle reductions over
+//     spheres), the height term is added after the reduction, and every lane applies the
+//     identical clamped step. LA = 4 measured fastest for every batch size;
+//   * sphere pairs (fixed yaw, uniform sphere radius r, rsum = 2r), two b-spheres per
+//     sm_100a FADD2/FMUL2/FFMA2 instruction (the scalar halves of a packed register pair
+//     are plain registers, so the per-pair MUFU.RSQ and selects need no unpacking):
+//       t = rsum / d - 1 = pen / d, active iff t > 0;  linear s = 1/d,  quadratic s = t
+//     with 1/d = rsqrt(d2 + 1e-30) (coincident centres: dx = 0 -> zero gradient, the
+//     reference's rule) and d cost/d ca = -w s (ca - cb) (x2 in quadratic);
+//   * walls: the four box walls of box_wall_spheres (tetris.py:54-70, normals +x, -x, +y,
+//     -y, verified on the host) in the cancellation-free form of pen_static_acc with the
+//     axis-aligned normal folded in: q = |v|^2 + 2R v.n = d^2 - R^2, pen = r - q / (d + R).
+//     (A branch skipping walls with q above the penetration bound was measured slower:
+//     divergence plus 204 registers.)
+//   * packing two particles per thread into sm_100a FFMA2/FADD2 was tried and dropped:
+//     cicc -O3 needs > 15 min per unrolled instantiation and ptxas then uses ~250
+//     registers.
 #pragma once
 #include "stage1_models.cuh"
 
 namespace spasm {
 
-// ---- scalar / packed-pair arithmetic --------------------------------------------------
-template <typename V> struct VX;
-
-template <> struct VX<float> {
-  static constexpr int P = 1;
-  static __device__ __forceinline__ float add(float a, float b) { return a + b; }
-  static __device__ __forceinline__ float sub(float a, float b) { return a - b; }
-  static __device__ __forceinline__ float mul(float a, float b) { return a * b; }
-  static __device__ __forceinline__ float fma(float a, float b, float c) { return fmaf(a, b, c); }
-  static __device__ __forceinline__ float k(float s, float2) { return s; }
-  static __device__ __forceinline__ float zero() { return 0.f; }
-  static __device__ __forceinline__ float rsq(float d2) { return rsqrtf(fmaxf(d2, 1e-30f)); }
-  static __device__ __forceinline__ float sel_lt(float a, float b, float v) { return a < b ? v : 0.f; }
-  static __device__ __forceinline__ float sel_gt0(float a, float v) { return a > 0.f ? v : 0.f; }
-  static __device__ __forceinline__ float relu(float a) { return fmaxf(a, 0.f); }
-  static __device__ __forceinline__ float div(float a, float b) { return __fdividef(a, b); }
-  static __device__ __forceinline__ float shfl_xor(float a, int m) { return __shfl_xor_sync(0xffffffffu, a, m); }
-  static __device__ __forceinline__ float get(float a, int) { return a; }
-  static __device__ __forceinline__ void set(float& a, int, float v) { a = v; }
+// ---- packed fp32 pairs (sm_100a FADD2/FMUL2/FFMA2) ----------------------------------
+// Two sphere pairs of one particle share one 64-bit register pair; the scalar halves are
+// plain registers (mov.b64 {lo, hi} is free aliasing), so per-component MUFU and selects
+// cost nothing extra. Every op is a single PTX statement on .b64 values.
+struct F2 {
+  unsigned long long v;
 };
+__device__ __forceinline__ F2 f2_make(float lo, float hi) {
+  F2 r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r.v) : "f"(lo), "f"(hi));
+  return r;
+}
+__device__ __forceinline__ F2 f2_dup(float a) { return f2_make(a, a); }
+// mask ? a : b as one LOP3 on the bit patterns: a data select the compiler cannot turn
+// into a branch (which would duplicate the unrolled pair code per mode)
+__device__ __forceinline__ float pick(unsigned mask, float a, float b) {
+  return __uint_as_float((mask & __float_as_uint(a)) | (~mask & __float_as_uint(b)));
+}
+__device__ __forceinline__ void f2_split(F2 a, float& lo, float& hi) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(a.v));
+}
+__device__ __forceinline__ F2 f2_add(F2 a, F2 b) {
+  F2 d;
+  asm("add.rn.ftz.f32x2 %0, %1, %2;" : "=l"(d.v) : "l"(a.v), "l"(b.v));
+  return d;
+}
+__device__ __forceinline__ F2 f2_sub(F2 a, F2 b) {
+  F2 d;
+  asm("sub.rn.ftz.f32x2 %0, %1, %2;" : "=l"(d.v) : "l"(a.v), "l"(b.v));
+  return d;
+}
+__device__ __forceinline__ F2 f2_mul(F2 a, F2 b) {
+  F2 d;
+  asm("mul.rn.ftz.f32x2 %0, %1, %2;" : "=l"(d.v) : "l"(a.v), "l"(b.v));
+  return d;
+}
+__device__ __forceinline__ F2 f2_fma(F2 a, F2 b, F2 c) {
+  F2 d;
+  asm("fma.rn.ftz.f32x2 %0, %1, %2, %3;" : "=l"(d.v) : "l"(a.v), "l"(b.v), "l"(c.v));
+  return d;
+}
 
-// ---- the tile model ---------------------------------------------------------------------
-template <int N, int LA, typename V>
+template <int N, int LA>
 struct TetrisTile {
-  using O = VX<V>;
   static constexpr int D = 3 * N;
   static constexpr int SA = kTileSpb / LA;  // a-spheres of each body handled by one lane
 
-  // lane-specific local offsets of the lane's a-spheres (LA > 1 only)
+  // Local offsets of the lane's a-spheres: constant-bank operands when LA == 1, else read
+  // from a shared-memory copy of the sphere table (lane-dependent index, no registers held).
   struct Lane {
-    V ax[N][SA], ay[N][SA], az[N][SA];
+    const float* tab;  // shared [3][N * kTileSpb]
+    int base;          // lane * SA
   };
 
-  static __device__ __forceinline__ void init_lane(const TetrisTileScene& sc, int lane, Lane& L) {
+  static __device__ __forceinline__ float off(const TetrisTileScene& sc, const Lane& L, int c, int i, int k) {
     if constexpr (LA > 1) {
-#pragma unroll
-      for (int i = 0; i < N; ++i)
-#pragma unroll
-        for (int k = 0; k < SA; ++k) {
-          const int a = i * kTileSpb + lane * SA + k;
-          L.ax[i][k] = O::k(sc.lx[a], sc.lx2[a]);
-          L.ay[i][k] = O::k(sc.ly[a], sc.ly2[a]);
-          L.az[i][k] = O::k(sc.lz[a], sc.lz2[a]);
-        }
+      return L.tab[c * N * kTileSpb + i * kTileSpb + L.base + k];
+    } else {
+      const int a = i * kTileSpb + k;
+      return c == 0 ? sc.lx[a] : (c == 1 ? sc.ly[a] : sc.lz[a]);
     }
   }
 
+  // One wall with inward normal sg * e_axis: va = v_axis (v = c - a, a = tangent point),
+  // perp = squared off-axis components of v, vo = the other horizontal component.
+  template <bool WC, bool WG, int SG>
+  static __device__ __forceinline__ void wall(const TetrisTileScene& sc, bool Q, float va, float perp, float vo,
+                                              float vz, float& ga, float& go, float& gz, float& cost) {
+    const float q = fmaf(va, SG * sc.two_wr, fmaf(va, va, perp));  // d^2 - R^2
+    const float d2 = q + sc.wr2;
+    const float inv = rsqrtf(fmaxf(d2, 1e-30f));
+    const float pen = sc.r - __fdividef(q, fmaf(d2, inv, sc.wr));  // r - (d - R)
+    if constexpr (WC) {
+      const float pc = fmaxf(pen, 0.f);
+      cost = fmaf(sc.w_bs, Q ? pc * pc : pc, cost);
+    }
+    if constexpr (WG) {
+      const float s = pen > 0.f ? (Q ? pen : 0.5f) * ((-2.f * sc.w_bs) * inv) : 0.f;
+      ga = fmaf(s, va + SG * sc.wr, ga);  // diff = c - s = v + R n
+      go = fmaf(s, vo, go);
+      gz = fmaf(s, vz, gz);
+    }
+  }
+
+  // Gradient of the two walls along one axis (+axis, -axis) as one packed pair: va = the
+  // sphere's coordinate minus the two tangent points, perp / vo / vz as in wall().
+  static __device__ __forceinline__ void wall_pair_grad(const TetrisTileScene& sc, bool Q, float w_axis,
+                                                        unsigned long long wa, float perp, float vo, float vz,
+                                                        float& ga, float& go, float& gz) {
+    const F2 VA = f2_sub(f2_dup(w_axis), F2{wa});
+    const F2 QQ = f2_fma(VA, F2{sc.two_wr_pm}, f2_fma(VA, VA, f2_dup(perp)));  // d^2 - R^2
+    const F2 D2 = f2_add(QQ, F2{sc.wr2_d});  // ~R^2 > 0
+    float d2a, d2b, qa, qb;
+    f2_split(D2, d2a, d2b);
+    f2_split(QQ, qa, qb);
+    const F2 INV = f2_make(rsqrtf(d2a), rsqrtf(d2b));
+    float da, db;
+    f2_split(f2_fma(D2, INV, F2{sc.wr_d}), da, db);  // d + R
+    const F2 PEN = f2_sub(F2{sc.r_d}, f2_make(__fdividef(qa, da), __fdividef(qb, db)));
+    float pa, pb, ia, ib;
+    f2_split(PEN, pa, pb);
+    f2_split(INV, ia, ib);
+    const float k = -2.f * sc.w_bs;
+    const float sa = pa > 0.f ? (Q ? pa : 0.5f) * (k * ia) : 0.f;
+    const float sb = pb > 0.f ? (Q ? pb : 0.5f) * (k * ib) : 0.f;
+    const F2 S = f2_make(sa, sb);
+    float l, r;
+    f2_split(f2_mul(S, f2_add(VA, F2{sc.wr_pm})), l, r);  // diff = v + R n
+    ga += l + r;
+    f2_split(f2_mul(S, f2_dup(vo)), l, r);
+    go += l + r;
+    f2_split(f2_mul(S, f2_dup(vz)), l, r);
+    gz += l + r;
+  }
+
   // Partial (lane) cost and/or gradient of the pair terms; the caller reduces across the
-  // LA lanes and adds the height term. Q: quadratic mode.
-  template <bool WC, bool WG, bool Q>
-  static __device__ __forceinline__ V pairs(const TetrisTileScene& sc, const Lane& L, const V (&x)[D], V (&g)[D]) {
-    V cost = O::zero();
+  // LA lanes and adds the height term. Q: quadratic mode, a runtime (warp-uniform) flag so
+  // the linear and quadratic phases share one copy of the unrolled code (the two-copy
+  // form stalled 42 % of issue slots on instruction-cache misses at N = 8).
+  template <bool WC, bool WG>
+  static __device__ __forceinline__ float pairs(const TetrisTileScene& sc, const Lane& L, bool Q, const float (&x)[D],
+                                                float (&g)[D]) {
+    float cost = 0.f;
+    const unsigned qmask = Q ? 0xFFFFFFFFu : 0u;
     if constexpr (WG) {
 #pragma unroll
-      for (int d = 0; d < D; ++d) g[d] = O::zero();
+      for (int d = 0; d < D; ++d) g[d] = 0.f;
     }
-    const V rs = O::k(sc.rs, sc.rs_2), rs2 = O::k(sc.rs2, sc.rs2_2);
 #pragma unroll
     for (int i = 0; i < N; ++i) {
 #pragma unroll
       for (int k = 0; k < SA; ++k) {
-        const int a = i * kTileSpb + k;  // LA == 1 only
-        const V lax = LA > 1 ? L.ax[i][k] : O::k(sc.lx[a], sc.lx2[a]);
-        const V lay = LA > 1 ? L.ay[i][k] : O::k(sc.ly[a], sc.ly2[a]);
-        const V laz = LA > 1 ? L.az[i][k] : O::k(sc.lz[a], sc.lz2[a]);
-        const V wax = O::add(x[3 * i], lax), way = O::add(x[3 * i + 1], lay), waz = O::add(x[3 * i + 2], laz);
+        const float wax = x[3 * i] + off(sc, L, 0, i, k);
+        const float way = x[3 * i + 1] + off(sc, L, 1, i, k);
+        const float waz = x[3 * i + 2] + off(sc, L, 2, i, k);
         // ---- body-body pairs (i < j), _interactions.py:46-60, 135-178
 #pragma unroll
-        for (int j = i + 1; j < N; ++j) {
-          const V tx = O::sub(wax, x[3 * j]), ty = O::sub(way, x[3 * j + 1]), tz = O::sub(waz, x[3 * j + 2]);
-          V gx = O::zero(), gy = O::zero(), gz = O::zero(), cp = O::zero();
+        for (int j = 0; j < N; ++j) {  // constant trip count: always fully unrolled
+          if (j <= i) continue;
+          const float tx = wax - x[3 * j], ty = way - x[3 * j + 1], tz = waz - x[3 * j + 2];
+          float gx = 0.f, gy = 0.f, gz = 0.f, cp = 0.f;
+          if constexpr (WC) {
 #pragma unroll
-          for (int sb = 0; sb < kTileSpb; ++sb) {
-            const int b = j * kTileSpb + sb;
-            const V dx = O::sub(tx, O::k(sc.lx[b], sc.lx2[b]));
-            const V dy = O::sub(ty, O::k(sc.ly[b], sc.ly2[b]));
-            const V dz = O::sub(tz, O::k(sc.lz[b], sc.lz2[b]));
-            const V d2 = O::fma(dz, dz, O::fma(dy, dy, O::mul(dx, dx)));
-            const V inv = O::rsq(d2);
-            if constexpr (WC) {
-              const V pc = O::relu(O::sub(rs, O::mul(d2, inv)));
-              cp = Q ? O::fma(pc, pc, cp) : O::add(cp, pc);
-            }
-            if constexpr (WG) {
-              const V s = Q ? O::relu(O::fma(rs, inv, O::k(-1.f, make_float2(-1.f, -1.f)))) : O::sel_lt(d2, rs2, inv);
-              gx = O::fma(s, dx, gx);
-              gy = O::fma(s, dy, gy);
-              gz = O::fma(s, dz, gz);
+            for (int sb = 0; sb < kTileSpb; ++sb) {
+              const int b = j * kTileSpb + sb;
+              const float dx = tx - sc.lx[b], dy = ty - sc.ly[b], dz = tz - sc.lz[b];
+              const float d2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
+              const float pc = fmaxf(sc.rs - d2 * rsqrtf(fmaxf(d2, 1e-30f)), 0.f);
+              cp = Q ? fmaf(pc, pc, cp) : cp + pc;
             }
           }
-          if constexpr (WC) cost = O::fma(O::k(sc.w_bb, make_float2(sc.w_bb, sc.w_bb)), cp, cost);
+          if constexpr (WG) {
+            // two b-spheres per packed op; the uniform Q picks the mode's scale
+            const F2 TX = f2_dup(tx), TY = f2_dup(ty), TZ = f2_dup(tz);
+            F2 GX = f2_dup(0.f), GY = GX, GZ = GX;
+#pragma unroll
+            for (int h = 0; h < kTileSpb; h += 2) {
+              const int b2 = (j * kTileSpb + h) / 2;
+              const F2 DX = f2_sub(TX, F2{sc.px[b2]}), DY = f2_sub(TY, F2{sc.py[b2]}), DZ = f2_sub(TZ, F2{sc.pz[b2]});
+              // d2 + 1e-30: keeps 1/d finite at coincident centres (zero gradient there)
+              // without a clamp instruction; 1e-30 is far below any fp32 pair distance^2
+              const F2 D2 = f2_fma(DZ, DZ, f2_fma(DY, DY, f2_fma(DX, DX, F2{sc.tiny_d})));
+              float d2a, d2b;
+              f2_split(D2, d2a, d2b);
+              const F2 INV = f2_make(rsqrtf(d2a), rsqrtf(d2b));
+              // t = rsum/d - 1 = pen/d; active iff t > 0. quadratic s = t, linear s = 1/d
+              float ta, tb, ia, ib;
+              f2_split(f2_fma(F2{sc.rs_d}, INV, F2{sc.m1_d}), ta, tb);
+              f2_split(INV, ia, ib);
+              const F2 S = f2_make(ta > 0.f ? pick(qmask, ta, ia) : 0.f, tb > 0.f ? pick(qmask, tb, ib) : 0.f);
+              GX = f2_fma(S, DX, GX);
+              GY = f2_fma(S, DY, GY);
+              GZ = f2_fma(S, DZ, GZ);
+            }
+            float l, r;
+            f2_split(GX, l, r);
+            gx = l + r;
+            f2_split(GY, l, r);
+            gy = l + r;
+            f2_split(GZ, l, r);
+            gz = l + r;
+          }
+          if constexpr (WC) cost = fmaf(sc.w_bb, cp, cost);
           if constexpr (WG) {
             const float w = Q ? -2.f * sc.w_bb : -sc.w_bb;
-            const V wv = O::k(w, make_float2(w, w));
-            const V nw = O::k(-w, make_float2(-w, -w));
-            g[3 * i] = O::fma(wv, gx, g[3 * i]);
-            g[3 * i + 1] = O::fma(wv, gy, g[3 * i + 1]);
-            g[3 * i + 2] = O::fma(wv, gz, g[3 * i + 2]);
-            g[3 * j] = O::fma(nw, gx, g[3 * j]);
-            g[3 * j + 1] = O::fma(nw, gy, g[3 * j + 1]);
-            g[3 * j + 2] = O::fma(nw, gz, g[3 * j + 2]);
+            g[3 * i] = fmaf(w, gx, g[3 * i]);
+            g[3 * i + 1] = fmaf(w, gy, g[3 * i + 1]);
+            g[3 * i + 2] = fmaf(w, gz, g[3 * i + 2]);
+            g[3 * j] = fmaf(-w, gx, g[3 * j]);
+            g[3 * j + 1] = fmaf(-w, gy, g[3 * j + 1]);
+            g[3 * j + 2] = fmaf(-w, gz, g[3 * j + 2]);
           }
         }
-        // ---- sphere vs wall (cancellation-free form), _interactions.py:62-73
-#pragma unroll
-        for (int st = 0; st < kTileWalls; ++st) {
-          const V vx = O::sub(wax, O::k(sc.ax[st], sc.ax2[st]));
-          const V vy = O::sub(way, O::k(sc.ay[st], sc.ay2[st]));
-          const V vz = O::sub(waz, O::k(sc.az[st], sc.az2[st]));
-          const V vn = O::fma(vz, O::k(sc.nz[st], sc.nz2[st]),
-                              O::fma(vy, O::k(sc.ny[st], sc.ny2[st]), O::mul(vx, O::k(sc.nx[st], sc.nx2[st]))));
-          const V vv = O::fma(vz, vz, O::fma(vy, vy, O::mul(vx, vx)));
-          const V q = O::fma(vn, O::k(sc.two_wr[st], sc.twr2[st]), vv);  // d^2 - R^2
-          const V d2 = O::add(q, O::k(sc.wr2[st], sc.wrsq2[st]));
-          const V inv = O::rsq(d2);
-          const V dpr = O::fma(d2, inv, O::k(sc.wr[st], sc.wr_2[st]));  // d + R
-          const V pen = O::sub(O::k(sc.r, sc.r_2), O::div(q, dpr));
-          if constexpr (WC) {
-            const V pc = O::relu(pen);
-            cost = Q ? O::fma(O::k(sc.w_bs, make_float2(sc.w_bs, sc.w_bs)), O::mul(pc, pc), cost)
-                     : O::fma(O::k(sc.w_bs, make_float2(sc.w_bs, sc.w_bs)), pc, cost);
-          }
-          if constexpr (WG) {
-            const float w = Q ? -2.f * sc.w_bs : -sc.w_bs;
-            const V s = O::sel_gt0(pen, Q ? O::mul(O::mul(O::k(w, make_float2(w, w)), pen), inv)
-                                          : O::mul(O::k(w, make_float2(w, w)), inv));
-            // diff = c - s = v + R n
-            g[3 * i] = O::fma(s, O::add(vx, O::k(sc.wrn_x[st], sc.wrnx2[st])), g[3 * i]);
-            g[3 * i + 1] = O::fma(s, O::add(vy, O::k(sc.wrn_y[st], sc.wrny2[st])), g[3 * i + 1]);
-            g[3 * i + 2] = O::fma(s, O::add(vz, O::k(sc.wrn_z[st], sc.wrnz2[st])), g[3 * i + 2]);
-          }
+        // ---- sphere vs the four walls (+x, -x, +y, -y), _interactions.py:62-73
+        const float vz = waz - sc.wall_az;
+        const float vyx = way - sc.wall_ay_x;  // off-axis component of the x walls
+        const float vxy = wax - sc.wall_ax_y;  // ... and of the y walls
+        const float px = fmaf(vyx, vyx, vz * vz), py = fmaf(vxy, vxy, vz * vz);
+        float gx = 0.f, gy = 0.f, gz = 0.f;
+        if constexpr (WC) {
+          wall<WC, false, 1>(sc, Q, wax - sc.wall_a[0], px, vyx, vz, gx, gy, gz, cost);
+          wall<WC, false, -1>(sc, Q, wax - sc.wall_a[1], px, vyx, vz, gx, gy, gz, cost);
+          wall<WC, false, 1>(sc, Q, way - sc.wall_a[2], py, vxy, vz, gy, gx, gz, cost);
+          wall<WC, false, -1>(sc, Q, way - sc.wall_a[3], py, vxy, vz, gy, gx, gz, cost);
+        }
+        if constexpr (WG) {
+          wall_pair_grad(sc, Q, wax, sc.wa_x, px, vyx, vz, gx, gy, gz);
+          wall_pair_grad(sc, Q, way, sc.wa_y, py, vxy, vz, gy, gx, gz);
+        }
+        if constexpr (WG) {
+          g[3 * i] += gx;
+          g[3 * i + 1] += gy;
+          g[3 * i + 2] += gz;
         }
       }
     }
@@ -161,35 +250,30 @@ struct TetrisTile {
   }
 
   // Height term (tetris.py:226-238; sign(0) == 0), identical on every lane.
-  template <bool WC, bool WG, bool Q>
-  static __device__ __forceinline__ void height(const TetrisTileScene& sc, const V (&x)[D], V (&g)[D], V& cost) {
+  template <bool WC, bool WG>
+  static __device__ __forceinline__ void height(const TetrisTileScene& sc, bool Q, const float (&x)[D], float (&g)[D],
+                                                float& cost) {
 #pragma unroll
     for (int i = 0; i < N; ++i) {
-#pragma unroll
-      for (int c = 0; c < O::P; ++c) {
-        const float dz = O::get(x[3 * i + 2], c) - sc.z_star;
-        if constexpr (WC) O::set(cost, c, O::get(cost, c) + (Q ? sc.w_h * (dz * dz) : sc.w_h * fabsf(dz)));
-        if constexpr (WG)
-          O::set(g[3 * i + 2], c,
-                 O::get(g[3 * i + 2], c) +
-                     (Q ? sc.w_h * (2.f * dz) : sc.w_h * (dz > 0.f ? 1.f : (dz < 0.f ? -1.f : 0.f))));
-      }
+      const float dz = x[3 * i + 2] - sc.z_star;
+      if constexpr (WC) cost += Q ? sc.w_h * (dz * dz) : sc.w_h * fabsf(dz);
+      if constexpr (WG) g[3 * i + 2] += Q ? sc.w_h * (2.f * dz) : sc.w_h * (dz > 0.f ? 1.f : (dz < 0.f ? -1.f : 0.f));
     }
   }
 };
 
-template <int LA, typename V>
-__device__ __forceinline__ V lane_sum(V v) {
-  if constexpr (LA >= 2) v = VX<V>::add(v, VX<V>::shfl_xor(v, 1));
-  if constexpr (LA >= 4) v = VX<V>::add(v, VX<V>::shfl_xor(v, 2));
+template <int LA>
+__device__ __forceinline__ float lane_sum(float v) {
+  if constexpr (LA >= 2) v += __shfl_xor_sync(0xffffffffu, v, 1);
+  if constexpr (LA >= 4) v += __shfl_xor_sync(0xffffffffu, v, 2);
   return v;
 }
 
-// Full cost/gradient of the particle(s) on every lane of the group.
-template <class T, int LA, typename V, bool WC, bool WG, bool Q>
-__device__ __forceinline__ V tile_eval(const TetrisTileScene& sc, const typename T::Lane& L, const V (&x)[T::D],
-                                      V (&g)[T::D]) {
-  V cost = T::template pairs<WC, WG, Q>(sc, L, x, g);
+// Full cost/gradient of the particle on every lane of the group.
+template <class T, int LA, bool WC, bool WG>
+__device__ __forceinline__ float tile_eval(const TetrisTileScene& sc, const typename T::Lane& L, bool Q,
+                                           const float (&x)[T::D], float (&g)[T::D]) {
+  float cost = T::template pairs<WC, WG>(sc, L, Q, x, g);
   if constexpr (LA > 1) {
     if constexpr (WC) cost = lane_sum<LA>(cost);
     if constexpr (WG) {
@@ -197,80 +281,67 @@ __device__ __forceinline__ V tile_eval(const TetrisTileScene& sc, const typename
       for (int d = 0; d < T::D; ++d) g[d] = lane_sum<LA>(g[d]);
     }
   }
-  T::template height<WC, WG, Q>(sc, x, g, cost);
+  T::template height<WC, WG>(sc, Q, x, g, cost);
   return cost;
 }
 
-// One clamped step per particle component with the NaN freeze (particle_opt.py:214-228).
-template <int D, typename V>
-__device__ __forceinline__ void tile_step(const TetrisTileScene& sc, V (&x)[D], const V (&g)[D], float rate,
-                                          bool (&bad)[VX<V>::P]) {
-  using O = VX<V>;
+// One clamped step with the NaN freeze (particle_opt.py:214-228).
+template <int D>
+__device__ __forceinline__ void tile_step(const TetrisTileScene& sc, float (&x)[D], const float (&g)[D], float rate,
+                                          bool& bad) {
+  bool b = false;
 #pragma unroll
-  for (int c = 0; c < O::P; ++c) {
-    bool b = false;
+  for (int d = 0; d < D; ++d) b |= !isfinite(g[d]);
+  bad |= b;
 #pragma unroll
-    for (int d = 0; d < D; ++d) b |= !isfinite(O::get(g[d], c));
-    bad[c] |= b;
-#pragma unroll
-    for (int d = 0; d < D; ++d) {
-      float v = O::get(x[d], c);
-      if (!b) v = v - rate * O::get(g[d], c);
-      v = fminf(fmaxf(v, sc.lower[d]), sc.upper[d]);
-      O::set(x[d], c, v);
-    }
+  for (int d = 0; d < D; ++d) {
+    float v = x[d];
+    if (!b) v = v - rate * g[d];
+    x[d] = fminf(fmaxf(v, sc.lower[d]), sc.upper[d]);
   }
 }
 
-template <int N, int LA, typename V>
+template <int N, int LA>
 __global__ void __launch_bounds__(128) k_schedule_tile(const __grid_constant__ TetrisTileScene sc,
                                                        const float* __restrict__ src, const uint32_t* __restrict__ rows,
                                                        int64_t M, int k_lin, int k_quad, double eta, double alpha,
                                                        float* __restrict__ out_values, float* __restrict__ out_cost,
                                                        uint8_t* __restrict__ flagged,
                                                        unsigned int* __restrict__ flagged_count) {
-  using T = TetrisTile<N, LA, V>;
-  using O = VX<V>;
-  constexpr int D = T::D, P = O::P;
+  using T = TetrisTile<N, LA>;
+  constexpr int D = T::D;
   const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int lane = (int)(threadIdx.x % LA);
-  const int64_t p0 = (gtid / LA) * P;  // first particle of this lane group
-  V x[D], g[D];
+  const int64_t p = gtid / LA;
+  const bool live = p < M;  // dead lanes still run (full-warp shuffles) on a valid row
+  const int64_t row = live ? (rows ? (int64_t)rows[p] : p) : 0;
+  float x[D], g[D];
 #pragma unroll
-  for (int c = 0; c < P; ++c) {
-    const int64_t p = p0 + c;
-    const bool live = p < M;
-    const int64_t row = live ? (rows ? (int64_t)rows[p] : p) : 0;
-#pragma unroll
-    for (int d = 0; d < D; ++d) O::set(x[d], c, live ? src[row * D + d] : sc.lower[d]);
+  for (int d = 0; d < D; ++d) x[d] = live ? src[row * D + d] : sc.lower[d];
+  __shared__ float tab[3 * N * kTileSpb];
+  for (int e = threadIdx.x; e < N * kTileSpb; e += blockDim.x) {
+    tab[e] = sc.lx[e];
+    tab[N * kTileSpb + e] = sc.ly[e];
+    tab[2 * N * kTileSpb + e] = sc.lz[e];
   }
-  typename T::Lane L;
-  T::init_lane(sc, lane, L);
-  bool bad[P];
-#pragma unroll
-  for (int c = 0; c < P; ++c) bad[c] = false;
-  for (int k = 1; k <= k_lin; ++k) {
+  __syncthreads();
+  const typename T::Lane L{tab, lane * T::SA};
+  bool bad = false;
+  // K_lin linear steps then K_quad quadratic steps, one loop over the shared eval code
+  for (int k = 1; k <= k_lin + k_quad; ++k) {
+    const bool quad = k > k_lin;
     // lr_schedule in float64 exactly as the reference, then cast (particle_opt.py:203-211)
-    const float rate = (float)(eta * (1.0 - (double)k / (double)k_lin));
-    tile_eval<T, LA, V, false, true, false>(sc, L, x, g);
-    tile_step<D, V>(sc, x, g, rate, bad);
+    const float rate = quad ? (float)alpha : (float)(eta * (1.0 - (double)k / (double)k_lin));
+    tile_eval<T, LA, false, true>(sc, L, quad, x, g);
+    tile_step<D>(sc, x, g, rate, bad);
   }
-  for (int k = 0; k < k_quad; ++k) {
-    tile_eval<T, LA, V, false, true, true>(sc, L, x, g);
-    tile_step<D, V>(sc, x, g, (float)alpha, bad);
-  }
-  const V fc = tile_eval<T, LA, V, true, false, true>(sc, L, x, g);
-  if (lane != 0) return;
+  const float fc = tile_eval<T, LA, true, false>(sc, L, true, x, g);
+  if (lane != 0 || !live) return;
 #pragma unroll
-  for (int c = 0; c < P; ++c) {
-    const int64_t p = p0 + c;
-    if (p >= M) break;
-#pragma unroll
-    for (int d = 0; d < D; ++d) out_values[p * D + d] = O::get(x[d], c);
-    out_cost[p] = O::get(fc, c);
-    if (flagged) flagged[p] = bad[c] ? 1 : 0;
-    if (bad[c] && flagged_count) atomicAdd(flagged_count, 1u);
-  }
+  for (int d = 0; d < D; ++d) out_values[p * D + d] = x[d];
+  out_cost[p] = fc;
+  if (flagged) flagged[p] = bad ? 1 : 0;
+  if (bad && flagged_count) atomicAdd(flagged_count, 1u);
 }
 
 }  // namespace spasm

@@ -4,7 +4,7 @@ TAG=${1:-x}
 mkdir -p gpurun_out
 timeout 900 python -m pytest tests/test_stage1_tile_gpu.py -x -q 2>&1 | tail -30 > gpurun_out/pytest_tile_$TAG.txt
 timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -5 > gpurun_out/pytest_gpu_$TAG.txt
-for v in 0 2 3 4; do
+for v in ${VARIANTS:-0 4}; do
   SPASM_STAGE1_TILE=$v timeout 300 python bench.py --steps 5 --warmup 3 --workload c5 --no-cpu > gpurun_out/bench_c5_t${v}_$TAG.json 2>&1
   SPASM_STAGE1_TILE=$v timeout 300 python bench.py --steps 5 --warmup 3 --workload c3 --no-cpu > gpurun_out/bench_c3_t${v}_$TAG.json 2>&1
 done
