@@ -391,6 +391,7 @@ static void fill_tile(Model& m, int n_bodies, const int32_t* spb, const double* 
   t.tiny_d = pack(1e-30f, 1e-30f);
   t.w_bb = (float)wbb;
   t.w_bs = (float)wbs;
+  t.k_bs_d = pack(-2.f * t.w_bs, -2.f * t.w_bs);
   t.w_h = (float)wh;
   t.z_star = (float)zs;
   for (int d = 0; d < 3 * n_bodies; ++d) {

@@ -79,7 +79,7 @@ struct TetrisTileScene {
   // packed wall constants (x walls, y walls as f32x2 pairs): tangent coordinates (a0, a1),
   // (a2, a3); (2R, -2R); (R, -R); and duplicated R^2, R, r
   unsigned long long wa_x, wa_y, two_wr_pm, wr_pm, wr2_d, wr_d, r_d;
-  unsigned long long rs_d, m1_d, tiny_d;  // duplicated rsum, -1, 1e-30
+  unsigned long long rs_d, m1_d, tiny_d, k_bs_d;  // duplicated rsum, -1, 1e-30, -2 w_bs
   float r, rs, rs2;  // uniform sphere radius, rsum = 2r, rsum^2
   float w_bb, w_bs, w_h, z_star;
   float lower[kTileMaxBodies * 3], upper[kTileMaxBodies * 3];

@@ -114,14 +114,14 @@ struct TetrisTile {
     }
   }
 
-  // Gradient of the two walls along one axis (+axis, -axis) as one packed pair: va = the
-  // sphere's coordinate minus the two tangent points, perp / vo / vz as in wall().
-  static __device__ __forceinline__ void wall_pair_grad(const TetrisTileScene& sc, bool Q, float w_axis,
-                                                        unsigned long long wa, float perp, float vo, float vz,
-                                                        float& ga, float& go, float& gz) {
-    const F2 VA = f2_sub(f2_dup(w_axis), F2{wa});
-    const F2 QQ = f2_fma(VA, F2{sc.two_wr_pm}, f2_fma(VA, VA, f2_dup(perp)));  // d^2 - R^2
-    const F2 D2 = f2_add(QQ, F2{sc.wr2_d});  // ~R^2 > 0
+  // Gradient of the two walls along one axis (+axis, -axis) as one packed pair: VA = the
+  // sphere's coordinate minus the two tangent points, PERP = squared off-axis part of v,
+  // VO / VZ = the other horizontal / the vertical component (duplicated). Accumulates
+  // into packed per-sphere accumulators GA (axis), GO (other), GZ.
+  static __device__ __forceinline__ void wall_pair_grad(const TetrisTileScene& sc, unsigned qmask, F2 VA, F2 PERP,
+                                                        F2 VO, F2 VZ, F2& GA, F2& GO, F2& GZ) {
+    const F2 QQ = f2_fma(VA, F2{sc.two_wr_pm}, f2_fma(VA, VA, PERP));  // d^2 - R^2
+    const F2 D2 = f2_add(QQ, F2{sc.wr2_d});                           // ~R^2 > 0
     float d2a, d2b, qa, qb;
     f2_split(D2, d2a, d2b);
     f2_split(QQ, qa, qb);
@@ -129,20 +129,15 @@ struct TetrisTile {
     float da, db;
     f2_split(f2_fma(D2, INV, F2{sc.wr_d}), da, db);  // d + R
     const F2 PEN = f2_sub(F2{sc.r_d}, f2_make(__fdividef(qa, da), __fdividef(qb, db)));
-    float pa, pb, ia, ib;
+    float pa, pb;
     f2_split(PEN, pa, pb);
-    f2_split(INV, ia, ib);
-    const float k = -2.f * sc.w_bs;
-    const float sa = pa > 0.f ? (Q ? pa : 0.5f) * (k * ia) : 0.f;
-    const float sb = pb > 0.f ? (Q ? pb : 0.5f) * (k * ib) : 0.f;
-    const F2 S = f2_make(sa, sb);
-    float l, r;
-    f2_split(f2_mul(S, f2_add(VA, F2{sc.wr_pm})), l, r);  // diff = v + R n
-    ga += l + r;
-    f2_split(f2_mul(S, f2_dup(vo)), l, r);
-    go += l + r;
-    f2_split(f2_mul(S, f2_dup(vz)), l, r);
-    gz += l + r;
+    // linear: -w / d; quadratic: -2 w pen / d  (k = -2w, factor 0.5 or pen)
+    float sa, sb;
+    f2_split(f2_mul(f2_mul(f2_make(pick(qmask, pa, 0.5f), pick(qmask, pb, 0.5f)), INV), F2{sc.k_bs_d}), sa, sb);
+    const F2 S = f2_make(pa > 0.f ? sa : 0.f, pb > 0.f ? sb : 0.f);
+    GA = f2_fma(S, f2_add(VA, F2{sc.wr_pm}), GA);  // diff = c - s = v + R n
+    GO = f2_fma(S, VO, GO);
+    GZ = f2_fma(S, VZ, GZ);
   }
 
   // Partial (lane) cost and/or gradient of the pair terms; the caller reduces across the
@@ -236,8 +231,17 @@ struct TetrisTile {
           wall<WC, false, -1>(sc, Q, way - sc.wall_a[3], py, vxy, vz, gy, gx, gz, cost);
         }
         if constexpr (WG) {
-          wall_pair_grad(sc, Q, wax, sc.wa_x, px, vyx, vz, gx, gy, gz);
-          wall_pair_grad(sc, Q, way, sc.wa_y, py, vxy, vz, gy, gx, gz);
+          F2 GX = f2_dup(0.f), GY = GX, GZ = GX;
+          const F2 VZ = f2_dup(vz);
+          wall_pair_grad(sc, qmask, f2_sub(f2_dup(wax), F2{sc.wa_x}), f2_dup(px), f2_dup(vyx), VZ, GX, GY, GZ);
+          wall_pair_grad(sc, qmask, f2_sub(f2_dup(way), F2{sc.wa_y}), f2_dup(py), f2_dup(vxy), VZ, GY, GX, GZ);
+          float l, r;
+          f2_split(GX, l, r);
+          gx = l + r;
+          f2_split(GY, l, r);
+          gy = l + r;
+          f2_split(GZ, l, r);
+          gz = l + r;
         }
         if constexpr (WG) {
           g[3 * i] += gx;
@@ -302,7 +306,7 @@ __device__ __forceinline__ void tile_step(const TetrisTileScene& sc, float (&x)[
 }
 
 template <int N, int LA>
-__global__ void __launch_bounds__(128) k_schedule_tile(const __grid_constant__ TetrisTileScene sc,
+__global__ void __launch_bounds__(128, 4) k_schedule_tile(const __grid_constant__ TetrisTileScene sc,
                                                        const float* __restrict__ src, const uint32_t* __restrict__ rows,
                                                        int64_t M, int k_lin, int k_quad, double eta, double alpha,
                                                        float* __restrict__ out_values, float* __restrict__ out_cost,
