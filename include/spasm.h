@@ -50,9 +50,9 @@ typedef struct spasm_model spasm_model; /* opaque placement cost model (scene ta
 const char* spasm_last_error(void);
 int spasm_version(void);
 /* Process-wide tuning switches (not in the reference; results stay within the parity
- * tolerances under every setting). "stage1_tile": -1 auto (default), 0 = generic stage-1
- * descent kernel only, 1..4 = force the fp32 tetris tile variant (packed pairs / 1, 2, 4
- * lanes per particle; stage1_tile.cuh). */
+ * tolerances under every setting). "stage1_tile": -1 auto (default: on), 0 = generic
+ * stage-1 kernels only, 1..4 = on (the fp32 tetris tile kernels, 4 lanes per particle;
+ * stage1_tile.cuh). */
 int spasm_set_option(const char* key, int value);
 
 /* ---- model construction ------------------------------------------------------

@@ -17,6 +17,11 @@ int launch_schedule_tile(const Model& m, const float* src, const uint32_t* rows,
                          double eta, double alpha, float* out_values, float* out_cost, uint8_t* flagged,
                          unsigned int* flagged_count, cudaStream_t s);
 
+// fp32 tetris tile sample + evaluate (stage1tile_f32.cu); returns -1 when not applicable.
+int launch_sample_eval_tile(const Model& m, const Pcg64State& st, int64_t row_offset, int64_t rows_n,
+                            const double* warm, int64_t n_warm, int use_philox, uint64_t seed, uint32_t restart,
+                            float* values, uint32_t* keys, uint32_t* idx, cudaStream_t s);
+
 inline int pick_block(int64_t P, size_t per_thread_bytes) {
   int bs = 128;
   if (P < (int64_t)kNumSMs * 128 * 2) bs = 64;
@@ -100,6 +105,11 @@ int launch_sample_eval(const Model& m, const Pcg64State& st, int64_t row_offset,
                        int64_t n_warm, int use_philox, uint64_t seed, uint32_t restart, R* values,
                        typename KeyOf<R>::type* keys, uint32_t* idx, cudaStream_t s) {
   if (N <= 0) return SPASM_OK;
+  if constexpr (std::is_same<R, float>::value) {
+    const int r = launch_sample_eval_tile(m, st, row_offset, N, warm, n_warm, use_philox, seed, restart, values, keys,
+                                          idx, s);
+    if (r != -1) return r;
+  }
   return dispatch_model<R>(m, [&](auto e, const auto& sc) -> int {
     using E = decltype(e);
     const size_t per = (size_t)(sc.dim + E::scratch_per_thread(sc)) * sizeof(R);

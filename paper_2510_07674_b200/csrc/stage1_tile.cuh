@@ -26,7 +26,7 @@
 //     cicc -O3 needs > 15 min per unrolled instantiation and ptxas then uses ~250
 //     registers.
 #pragma once
-#include "stage1_models.cuh"
+#include "stage1_kernels.cuh"
 
 namespace spasm {
 
@@ -93,27 +93,6 @@ struct TetrisTile {
     }
   }
 
-  // One wall with inward normal sg * e_axis: va = v_axis (v = c - a, a = tangent point),
-  // perp = squared off-axis components of v, vo = the other horizontal component.
-  template <bool WC, bool WG, int SG>
-  static __device__ __forceinline__ void wall(const TetrisTileScene& sc, bool Q, float va, float perp, float vo,
-                                              float vz, float& ga, float& go, float& gz, float& cost) {
-    const float q = fmaf(va, SG * sc.two_wr, fmaf(va, va, perp));  // d^2 - R^2
-    const float d2 = q + sc.wr2;
-    const float inv = rsqrtf(fmaxf(d2, 1e-30f));
-    const float pen = sc.r - __fdividef(q, fmaf(d2, inv, sc.wr));  // r - (d - R)
-    if constexpr (WC) {
-      const float pc = fmaxf(pen, 0.f);
-      cost = fmaf(sc.w_bs, Q ? pc * pc : pc, cost);
-    }
-    if constexpr (WG) {
-      const float s = pen > 0.f ? (Q ? pen : 0.5f) * ((-2.f * sc.w_bs) * inv) : 0.f;
-      ga = fmaf(s, va + SG * sc.wr, ga);  // diff = c - s = v + R n
-      go = fmaf(s, vo, go);
-      gz = fmaf(s, vz, gz);
-    }
-  }
-
   // Gradient of the two walls along one axis (+axis, -axis) as one packed pair: VA = the
   // sphere's coordinate minus the two tangent points, PERP = squared off-axis part of v,
   // VO / VZ = the other horizontal / the vertical component (duplicated). Accumulates
@@ -138,6 +117,19 @@ struct TetrisTile {
     GA = f2_fma(S, f2_add(VA, F2{sc.wr_pm}), GA);  // diff = c - s = v + R n
     GO = f2_fma(S, VO, GO);
     GZ = f2_fma(S, VZ, GZ);
+  }
+
+  // Cost of the two walls along one axis as one packed pair: w * pen+ (or pen+^2).
+  static __device__ __forceinline__ float wall_pair_cost(const TetrisTileScene& sc, bool Q, F2 VA, F2 PERP) {
+    const F2 QQ = f2_fma(VA, F2{sc.two_wr_pm}, f2_fma(VA, VA, PERP));  // d^2 - R^2
+    const F2 D2 = f2_add(QQ, F2{sc.wr2_d});
+    float d2a, d2b, qa, qb;
+    f2_split(D2, d2a, d2b);
+    f2_split(QQ, qa, qb);
+    float da, db;
+    f2_split(f2_fma(D2, f2_make(rsqrtf(d2a), rsqrtf(d2b)), F2{sc.wr_d}), da, db);  // d + R
+    const float pa = fmaxf(sc.r - __fdividef(qa, da), 0.f), pb = fmaxf(sc.r - __fdividef(qb, db), 0.f);
+    return sc.w_bs * (Q ? fmaf(pa, pa, pb * pb) : pa + pb);
   }
 
   // Partial (lane) cost and/or gradient of the pair terms; the caller reduces across the
@@ -166,15 +158,24 @@ struct TetrisTile {
           if (j <= i) continue;
           const float tx = wax - x[3 * j], ty = way - x[3 * j + 1], tz = waz - x[3 * j + 2];
           float gx = 0.f, gy = 0.f, gz = 0.f, cp = 0.f;
-          if constexpr (WC) {
+          if constexpr (WC) {  // packed like the gradient path: pen = rsum - d
+            const F2 TX = f2_dup(tx), TY = f2_dup(ty), TZ = f2_dup(tz);
+            F2 CP = f2_dup(0.f);
 #pragma unroll
-            for (int sb = 0; sb < kTileSpb; ++sb) {
-              const int b = j * kTileSpb + sb;
-              const float dx = tx - sc.lx[b], dy = ty - sc.ly[b], dz = tz - sc.lz[b];
-              const float d2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
-              const float pc = fmaxf(sc.rs - d2 * rsqrtf(fmaxf(d2, 1e-30f)), 0.f);
-              cp = Q ? fmaf(pc, pc, cp) : cp + pc;
+            for (int h = 0; h < kTileSpb; h += 2) {
+              const int b2 = (j * kTileSpb + h) / 2;
+              const F2 DX = f2_sub(TX, F2{sc.px[b2]}), DY = f2_sub(TY, F2{sc.py[b2]}), DZ = f2_sub(TZ, F2{sc.pz[b2]});
+              const F2 D2 = f2_fma(DZ, DZ, f2_fma(DY, DY, f2_fma(DX, DX, F2{sc.tiny_d})));
+              float d2a, d2b;
+              f2_split(D2, d2a, d2b);
+              float pa, pb;
+              f2_split(f2_sub(F2{sc.rs_d}, f2_mul(D2, f2_make(rsqrtf(d2a), rsqrtf(d2b)))), pa, pb);
+              const F2 PC = f2_make(fmaxf(pa, 0.f), fmaxf(pb, 0.f));
+              CP = Q ? f2_fma(PC, PC, CP) : f2_add(CP, PC);
             }
+            float l, r;
+            f2_split(CP, l, r);
+            cp = l + r;
           }
           if constexpr (WG) {
             // two b-spheres per packed op; the uniform Q picks the mode's scale
@@ -225,10 +226,8 @@ struct TetrisTile {
         const float px = fmaf(vyx, vyx, vz * vz), py = fmaf(vxy, vxy, vz * vz);
         float gx = 0.f, gy = 0.f, gz = 0.f;
         if constexpr (WC) {
-          wall<WC, false, 1>(sc, Q, wax - sc.wall_a[0], px, vyx, vz, gx, gy, gz, cost);
-          wall<WC, false, -1>(sc, Q, wax - sc.wall_a[1], px, vyx, vz, gx, gy, gz, cost);
-          wall<WC, false, 1>(sc, Q, way - sc.wall_a[2], py, vxy, vz, gy, gx, gz, cost);
-          wall<WC, false, -1>(sc, Q, way - sc.wall_a[3], py, vxy, vz, gy, gx, gz, cost);
+          cost += wall_pair_cost(sc, Q, f2_sub(f2_dup(wax), F2{sc.wa_x}), f2_dup(px)) +
+                  wall_pair_cost(sc, Q, f2_sub(f2_dup(way), F2{sc.wa_y}), f2_dup(py));
         }
         if constexpr (WG) {
           F2 GX = f2_dup(0.f), GY = GX, GZ = GX;
@@ -346,6 +345,35 @@ __global__ void __launch_bounds__(128, 4) k_schedule_tile(const __grid_constant_
   out_cost[p] = fc;
   if (flagged) flagged[p] = bad ? 1 : 0;
   if (bad && flagged_count) atomicAdd(flagged_count, 1u);
+}
+
+// LINEAR cost + ranking key of freshly sampled rows (particle_opt.py:326-330), LA lanes per
+// row like the schedule; the rows come from k_sample (stage1_kernels.cuh).
+template <int N, int LA>
+__global__ void __launch_bounds__(128) k_keys_tile(const __grid_constant__ TetrisTileScene sc,
+                                                   const float* __restrict__ values, int64_t row_offset, int64_t rows_n,
+                                                   uint32_t* __restrict__ keys, uint32_t* __restrict__ idx) {
+  using T = TetrisTile<N, LA>;
+  constexpr int D = T::D;
+  const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int lane = (int)(threadIdx.x % LA);
+  const int64_t p = gtid / LA;
+  const bool live = p < rows_n;
+  __shared__ float tab[3 * N * kTileSpb];
+  for (int e = threadIdx.x; e < N * kTileSpb; e += blockDim.x) {
+    tab[e] = sc.lx[e];
+    tab[N * kTileSpb + e] = sc.ly[e];
+    tab[2 * N * kTileSpb + e] = sc.lz[e];
+  }
+  __syncthreads();
+  float x[D], g[D];
+#pragma unroll
+  for (int d = 0; d < D; ++d) x[d] = live ? values[p * D + d] : sc.lower[d];
+  const typename T::Lane L{tab, lane * T::SA};
+  const float c = tile_eval<T, LA, true, false>(sc, L, false, x, g);
+  if (lane != 0 || !live) return;
+  keys[p] = order_key(c);
+  idx[p] = (uint32_t)(row_offset + p);
 }
 
 }  // namespace spasm
