@@ -21,6 +21,7 @@
 #pragma once
 #include "coop.cuh"
 #include "stage1_models.cuh"
+#include "twin_warp.cuh"
 
 namespace spasm {
 
@@ -32,30 +33,6 @@ struct NoTwin {
 template <typename R, int KIND> struct TwinSceneOf { using type = NoTwin<R>; };
 template <typename R> struct TwinSceneOf<R, 1> { using type = TetrisScene<R>; };
 template <typename R> struct TwinSceneOf<R, 2> { using type = TowerScene<R>; };
-
-template <typename R, int KIND, int SPB, bool WG, bool Q>
-__device__ __forceinline__ R twin_run_t(const typename TwinSceneOf<R, KIND>::type& ts, const R* rows, R* grad,
-                                        R* scr) {
-  if constexpr (KIND == 1) {
-    return TetrisEval<R, SPB, true>::template run<true, WG, Q>(ts, rows, grad, scr, 1);
-  } else if constexpr (KIND == 2) {
-    return TowerEval<R, true>::template run<true, WG, Q>(ts, rows, grad, scr, 1);
-  } else {
-    return R(0);
-  }
-}
-
-template <typename R, int KIND, int SPB>
-__device__ __forceinline__ R twin_run(const typename TwinSceneOf<R, KIND>::type& ts, const R* rows, R* grad, R* scr,
-                                      bool want_grad, bool quad) {
-  if (want_grad) {
-    return quad ? twin_run_t<R, KIND, SPB, true, true>(ts, rows, grad, scr)
-                : twin_run_t<R, KIND, SPB, true, false>(ts, rows, grad, scr);
-  }
-  return quad ? twin_run_t<R, KIND, SPB, false, true>(ts, rows, grad, scr)
-              : twin_run_t<R, KIND, SPB, false, false>(ts, rows, grad, scr);
-}
-
 
 constexpr int kMaxAlThreads = 512;  // 60 waypoint tiles + the aux warp; <= 128 registers
 constexpr int kXS = 8;  // row stride of x / g / unit in shared memory ([w][joint])
@@ -102,7 +79,7 @@ __host__ __device__ inline AlLayout al_layout(int B, int T, int J, int S, int SB
   L.seg = take(3 * B * r);  // psi | cp | sp
   L.rows = take(4 * B * r);
   L.gpose = take(4 * B * r);
-  L.scr = take((2 * B + 2) * r);
+  L.scr = take(twin_warp_scratch(B > 0 ? B : 1) * r);  // warp twin: per-lane gradient slots (twin_warp.cuh)
   L.pgsum = take(8 * B * r);
   L.red = take(4 * L.nwarps * r);
   L.scal = take(32 * r);
@@ -310,8 +287,8 @@ __device__ void al_eval(AlCtx<R>& C, const typename TwinSceneOf<R, KIND>::type& 
         }
       }
       __syncwarp();
+      R cpl = twin_warp<R, KIND, SPB>(tw, C.rows, C.gpose, C.scr, lane, want_grad, pquad);
       if (lane == 0) {
-        R cpl = twin_run<R, KIND, SPB>(tw, C.rows, C.gpose, C.scr, want_grad, pquad);
         if (sc.anchor) {
           for (int bb = 0; bb < B; ++bb) {
             const R wp = wrap_yaw(C.psi[bb]);
@@ -605,13 +582,15 @@ __device__ void al_validate(AlCtx<R>& C, const typename TwinSceneOf<R, KIND>::ty
   }
   __syncthreads();
   R worst = R(0);
-  if (is_aux && lane == 0) {
-    if (manip) {
-      R place = twin_run<R, KIND, SPB>(tw, C.rows, nullptr, C.scr, false, false);
+  if (is_aux && manip) {
+    R place = twin_warp<R, KIND, SPB>(tw, C.rows, nullptr, C.scr, lane, false, false);
+    if (lane == 0) {
       if (sc.anchor)
         for (int bb = 0; bb < B; ++bb) place += fabs(wrap_yaw(C.rows[4 * bb + 3]));
       worst = fmax(worst, place);
-    } else {
+    }
+  } else if (is_aux && lane == 0) {
+    {
       for (int k = 0; k < J; ++k) {
         worst = fmax(worst, fabs(C.x[0 * kXS + k] - sc.start[k]));
         worst = fmax(worst, fabs(C.x[(T - 1) * kXS + k] - sc.goal[k]));
