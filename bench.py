@@ -40,6 +40,9 @@ WORKLOADS = {
     "c2": ("tower3c", {}, False,
            "C2 3-block stacking with cuboid obstacles (sphere-grid cuboids), 16k particles, stage 1 + stage 2"),
     "c3": ("tetris5", {"n": 65536, "m": 8192}, True, "C3 Tetris packing, 5 objects, 64k particles, stage 1"),
+    "c4": ("tower6r", {"n": 16384, "m": 2048}, True,
+           "C4 reactive replanning: 6-block rearrangement, one sphere obstacle moving 3 cm per tick, each tick "
+           "warm-started from the previous placement, 16k particles, stage 1"),
     "c5": ("tetris8", {"n": 1 << 20, "m": 1 << 17}, True, "C5 8-object skeleton, 1M particles (M = N/8), stage 1"),
 }
 
@@ -244,6 +247,28 @@ def run_b200(args):
         return solve_scene(scene, seed=seed, solver_overrides=over, no_trajopt=stage1_only, precision=args.precision,
                            model=model, comm=comm)
 
+    replan = None
+    if args.workload == "c4":
+        # one step = one replan tick: move the obstacle, rebuild the scene/model, re-solve
+        # warm-started from the previous tick's placement (replan.py)
+        from paper_2510_07674_b200.problems.scenes import tower6r
+        from paper_2510_07674_b200.replan import obstacle_center
+
+        replan = {"tick": 0, "warm": None, "tick_ms": []}
+
+        def step(seed):  # noqa: F811
+            t0 = time.perf_counter()
+            k = replan["tick"]
+            replan["tick"] += 1
+            sc = load_scene(tower6r(obstacle_center=obstacle_center(k)))
+            mdl = as_cost_model(sc.problem, precision=args.precision)
+            sol = solve_scene(sc, seed=seed, solver_overrides=over, no_trajopt=True, precision=args.precision,
+                              model=mdl, warm_seeds=replan["warm"], comm=comm)
+            if sol.success:
+                replan["warm"] = sol.placement[None, :].copy()
+            replan["tick_ms"].append((time.perf_counter() - t0) * 1e3)
+            return sol
+
     seed0 = 0
     for i in range(args.warmup):
         step(seed0 + 100000 + i)
@@ -309,6 +334,12 @@ def run_b200(args):
         if world > 1:
             dist.destroy_process_group()
         return
+    replan_line = None
+    if replan is not None:
+        from paper_2510_07674_b200.replan import rate_sweep
+
+        replan_line = {**rate_sweep(replan["tick_ms"][args.warmup:]), "step_m": 0.03,
+                       "warm_started_ticks": args.steps, "note": "tick = obstacle move + scene/model rebuild + solve"}
     cpu = cpu_baseline(args) if (world == 1 and not args.no_cpu) else None
     D = model.dimension
     p_ret = cfg.p_return
@@ -345,6 +376,7 @@ def run_b200(args):
         "cpu_baseline": cpu,
         "clocks": clk,
         "gpu_launches": launches,
+        "replan": replan_line,
         "breakdown": {"stage1_ms_mean": statistics.mean(s.stats.get("stage1_ms", 0.0) for s in sols),
                       "al_device_ms_mean": statistics.mean(al_ms) if al_ms else None,
                       "stage2_outers_mean": statistics.mean(s.stats.get("stage2_outers", 0) for s in sols)},
