@@ -136,6 +136,11 @@ typedef struct {
   uint64_t seed;
   int32_t sampler;        /* SPASM_SAMPLER_* */
   int32_t n_traced;       /* 0 = no trace; else min(m, 4096) rows traced */
+  /* perf-mode particle update (north_star item 4; not in the reference). All zero = the
+   * reference's clamped gradient step (particle_opt.py:214-228), used by every parity path. */
+  int32_t update;         /* 0 = gradient step (reference), 1 = Adam scaled by the lr schedule */
+  float adam_beta1, adam_beta2, adam_eps;
+  float noise_sigma;      /* initial Gaussian noise std / bound width, annealed to 0 over K_lin */
 } spasm_solve_config;
 
 typedef struct {

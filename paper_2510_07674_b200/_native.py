@@ -48,6 +48,11 @@ class spasm_solve_config(ctypes.Structure):
         ("seed", c_uint64),
         ("sampler", c_int32),
         ("n_traced", c_int32),
+        ("update", c_int32),
+        ("adam_beta1", ctypes.c_float),
+        ("adam_beta2", ctypes.c_float),
+        ("adam_eps", ctypes.c_float),
+        ("noise_sigma", ctypes.c_float),
     ]
 
 

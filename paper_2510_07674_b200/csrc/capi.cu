@@ -119,7 +119,25 @@ static int validate_cfg(const spasm_solve_config* cfg) {
   SPASM_REQUIRE(cfg->p_return >= 1, "p_return must be >= 1");
   SPASM_REQUIRE(cfg->max_restarts >= 1, "max_restarts must be >= 1");
   SPASM_REQUIRE(cfg->n_traced >= 0 && cfg->n_traced <= cfg->m, "n_traced must be in [0, m]");
+  SPASM_REQUIRE(cfg->update == 0 || cfg->update == 1, "update must be 0 (gradient step) or 1 (Adam)");
+  SPASM_REQUIRE(cfg->noise_sigma >= 0.f, "noise_sigma must be >= 0");
+  if (cfg->update == 1)
+    SPASM_REQUIRE(cfg->adam_beta1 >= 0.f && cfg->adam_beta1 < 1.f && cfg->adam_beta2 >= 0.f && cfg->adam_beta2 < 1.f &&
+                      cfg->adam_eps > 0.f,
+                  "Adam needs 0 <= beta1, beta2 < 1 and eps > 0");
   return SPASM_OK;
+}
+
+StepRule step_rule(const spasm_solve_config& cfg, int restart) {
+  StepRule r;
+  r.adam = cfg.update;
+  r.b1 = cfg.adam_beta1;
+  r.b2 = cfg.adam_beta2;
+  r.eps = cfg.adam_eps;
+  r.noise = cfg.noise_sigma;
+  r.seed = cfg.seed;
+  r.restart = (uint32_t)restart;
+  return r;
 }
 
 template <typename R>
@@ -188,7 +206,7 @@ static int solve_impl(Model& m, const spasm_solve_config& cfg, const double* war
     const bool tr = trace_cost != nullptr && cfg.n_traced > 0;
     if ((r = launch_schedule<R>(m, values, top, cfg.m, cfg.k_lin, cfg.k_quad, cfg.eta_init, cfg.alpha, cfg.epsilon,
                                 opt_values, opt_cost, flagged, counters + 1, tr ? trace_cost : nullptr,
-                                tr ? trace_sat : nullptr, tr ? cfg.n_traced : 0, s)))
+                                tr ? trace_sat : nullptr, tr ? cfg.n_traced : 0, step_rule(cfg, restart), s)))
       return r;
     if (tr && trace_ids) {
       k_trace_ids<<<ceil_div(cfg.n_traced, 256), 256, 0, s>>>(top, cfg.n_traced, trace_ids);
@@ -583,7 +601,7 @@ int spasm_descent_schedule(const spasm_model* model, int dtype, const void* src,
                                                       eta_init, alpha, epsilon, static_cast<R*>(out_values),
                                                       static_cast<R*>(out_cost), flagged, flagged_count,
                                                       static_cast<R*>(trace_cost), trace_sat, n_traced,
-                                                      as_stream(stream)););
+                                                      StepRule{}, as_stream(stream)););
 }
 
 int64_t spasm_sort_workspace_bytes(int dtype, int64_t n) {

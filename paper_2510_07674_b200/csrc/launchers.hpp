@@ -33,7 +33,7 @@ int launch_sample_eval(const Model&, const Pcg64State&, int64_t, int64_t, const 
                        uint32_t, R*, typename KeyOf<R>::type*, uint32_t*, cudaStream_t);
 template <typename R>
 int launch_schedule(const Model&, const R*, const uint32_t*, int64_t, int, int, double, double, double, R*, R*,
-                    uint8_t*, unsigned int*, R*, uint8_t*, int, cudaStream_t);
+                    uint8_t*, unsigned int*, R*, uint8_t*, int, const StepRule&, cudaStream_t);
 template <typename R>
 int launch_sample(const Bounds64&, int, const Pcg64State&, int64_t, const uint32_t*, int64_t, const double*, int64_t,
                   int, uint64_t, uint32_t, R*, cudaStream_t);

@@ -85,4 +85,19 @@ struct TetrisTileScene {
   float lower[kTileMaxBodies * 3], upper[kTileMaxBodies * 3];
 };
 
+// Perf-mode particle update (north_star item 4; not in the reference). The default
+// (adam = 0, noise = 0) is the reference's clamped gradient step (particle_opt.py:214-228)
+// and every parity path uses it. adam: Adam moments with bias correction, scaled by the
+// reference's learning-rate schedule. noise: Gaussian perturbation with std
+// noise * (upper - lower) per dimension, annealed linearly to 0 over the linear phase,
+// drawn from Philox4x32-10 keyed by (seed, restart, particle, step).
+struct StepRule {
+  int adam;
+  float b1, b2, eps;
+  float noise;
+  uint64_t seed;
+  uint32_t restart;
+  __host__ __device__ bool is_reference() const { return adam == 0 && noise == 0.f; }
+};
+
 }  // namespace spasm

@@ -20,6 +20,8 @@
 
 namespace spasm {
 
+StepRule step_rule(const spasm_solve_config& cfg, int restart);  // capi.cu
+
 static size_t shard_align(size_t x) { return (x + 255) & ~(size_t)255; }
 
 struct ShardLayout {
@@ -203,7 +205,8 @@ static int shard_descend_impl(const Model& m, const spasm_solve_config& cfg, int
   if (r) return r;
   SPASM_CUDA_TRY(cudaMemsetAsync(counters, 0, 64, s));
   if ((r = launch_schedule<R>(m, opt_in, nullptr, ml, cfg.k_lin, cfg.k_quad, cfg.eta_init, cfg.alpha, cfg.epsilon,
-                              opt_values, opt_cost, flagged, counters + 1, nullptr, nullptr, 0, s)))
+                              opt_values, opt_cost, flagged, counters + 1, nullptr, nullptr, 0,
+                              step_rule(cfg, restart), s)))
     return r;
   if ((r = launch_sat_keys<R>(opt_cost, ml, cfg.epsilon, sk0, sv0, counters, s))) return r;
   bool in1 = false;

@@ -198,12 +198,54 @@ __global__ void k_step(R* __restrict__ values, const R* __restrict__ grad, int64
 // sampled batch so the selected rows never round-trip through a separate copy.
 // Trace (optional): per step, the active-mode cost and quadratic satisfaction of the
 // first n_traced particles (particle_opt.py:286-297).
+// Perf-mode update (StepRule, scene.cuh): Adam and/or annealed Philox noise. am/av hold the
+// Adam moments (column layout like x); t is the 1-based step count, p the batch row.
+template <typename R>
+__device__ __forceinline__ bool apply_step_rule(R* x, R* g, R* am, R* av, int D, int bs, R rate, const R* lower,
+                                                const R* upper, const StepRule& rule, int t, int64_t p, R sigma) {
+  bool bad = false;
+  for (int d = 0; d < D; ++d) bad |= !Math<R>::finite(g[d * bs]);
+  const R c1 = R(1) - (R)pow((double)rule.b1, (double)t), c2 = R(1) - (R)pow((double)rule.b2, (double)t);
+  const uint2 key = make_uint2((uint32_t)rule.seed, (uint32_t)(rule.seed >> 32));
+  R z[2] = {R(0), R(0)};
+  for (int d = 0; d < D; ++d) {
+    R v = x[d * bs];
+    if (!bad) {
+      R u = g[d * bs];
+      if (rule.adam) {
+        const R m = R(rule.b1) * am[d * bs] + (R(1) - R(rule.b1)) * u;
+        const R s2 = R(rule.b2) * av[d * bs] + (R(1) - R(rule.b2)) * u * u;
+        am[d * bs] = m;
+        av[d * bs] = s2;
+        u = (m / c1) / (Math<R>::sqrt_(s2 / c2) + R(rule.eps));
+      }
+      v = v - rate * u;
+      if (sigma > R(0)) {
+        if ((d & 1) == 0) {  // Box-Muller pair per two dimensions
+          const uint4 r4 = Philox4x32::gen(
+              make_uint4((uint32_t)p, (uint32_t)(p >> 32) ^ ((uint32_t)t << 8), rule.restart, 0x80000000u | (uint32_t)d),
+              key);
+          const double u1 = ((double)(r4.x >> 8) + 0.5) * (1.0 / 16777216.0);
+          const double u2 = (double)(r4.y >> 8) * (1.0 / 16777216.0);
+          const double rad = sqrt(-2.0 * log(u1));
+          z[0] = (R)(rad * cos(6.283185307179586 * u2));
+          z[1] = (R)(rad * sin(6.283185307179586 * u2));
+        }
+        v = v + sigma * (upper[d] - lower[d]) * z[d & 1];
+      }
+    }
+    v = v < lower[d] ? lower[d] : (v > upper[d] ? upper[d] : v);
+    x[d * bs] = v;
+  }
+  return bad;
+}
+
 template <class E, typename R, bool TRACE>
 __global__ void k_schedule(const typename E::Scene sc, const R* __restrict__ src, const uint32_t* __restrict__ rows,
                            int64_t M, int k_lin, int k_quad, double eta, double alpha, double eps,
                            R* __restrict__ out_values, R* __restrict__ out_cost, uint8_t* __restrict__ flagged,
                            unsigned int* __restrict__ flagged_count, R* __restrict__ trace_cost,
-                           uint8_t* __restrict__ trace_sat, int n_traced) {
+                           uint8_t* __restrict__ trace_sat, int n_traced, const StepRule rule) {
   const int bs = blockDim.x;
   const int D = sc.dim;
   R* base = particle_smem<R>(0);
@@ -215,13 +257,22 @@ __global__ void k_schedule(const typename E::Scene sc, const R* __restrict__ src
     R* x = base + threadIdx.x;
     R* g = base + (int64_t)D * bs + threadIdx.x;
     R* scr = base + (int64_t)2 * D * bs + threadIdx.x;
+    const bool ref = rule.is_reference();
+    R* am = base + (int64_t)(2 * D + E::scratch_per_thread(sc)) * bs + threadIdx.x;  // Adam moments (perf mode)
+    R* av = am + (int64_t)D * bs;
+    if (rule.adam)
+      for (int d = 0; d < D; ++d) am[d * bs] = av[d * bs] = R(0);
     bool bad = false;
     int step = 0;
     for (int k = 1; k <= k_lin; ++k) {
       // lr_schedule in float64 exactly as the reference, then cast (particle_opt.py:203-211)
       const R rate = (R)(eta * (1.0 - (double)k / (double)k_lin));
       E::template run<false, true, false>(sc, x, g, scr, bs);
-      bad |= apply_step<R>(x, g, D, bs, rate, sc.lower, sc.upper);
+      if (ref)
+        bad |= apply_step<R>(x, g, D, bs, rate, sc.lower, sc.upper);
+      else
+        bad |= apply_step_rule<R>(x, g, am, av, D, bs, rate, sc.lower, sc.upper, rule, step + 1, p,
+                                  R(rule.noise) * R(1.0 - (double)k / (double)k_lin));
       if constexpr (TRACE) {
         if (p < n_traced) {
           const R cl = E::template run<true, false, false>(sc, x, nullptr, scr, bs);
@@ -234,7 +285,10 @@ __global__ void k_schedule(const typename E::Scene sc, const R* __restrict__ src
     }
     for (int k = 0; k < k_quad; ++k) {
       E::template run<false, true, true>(sc, x, g, scr, bs);
-      bad |= apply_step<R>(x, g, D, bs, (R)alpha, sc.lower, sc.upper);
+      if (ref)
+        bad |= apply_step<R>(x, g, D, bs, (R)alpha, sc.lower, sc.upper);
+      else
+        bad |= apply_step_rule<R>(x, g, am, av, D, bs, (R)alpha, sc.lower, sc.upper, rule, step + 1, p, R(0));
       if constexpr (TRACE) {
         if (p < n_traced) {
           const R cq = E::template run<true, false, true>(sc, x, nullptr, scr, bs);

@@ -125,10 +125,11 @@ int launch_sample_eval(const Model& m, const Pcg64State& st, int64_t row_offset,
 template <typename R>
 int launch_schedule(const Model& m, const R* src, const uint32_t* rows, int64_t M, int k_lin, int k_quad,
                     double eta, double alpha, double eps, R* out_values, R* out_cost, uint8_t* flagged,
-                    unsigned int* flagged_count, R* trace_cost, uint8_t* trace_sat, int n_traced, cudaStream_t s) {
+                    unsigned int* flagged_count, R* trace_cost, uint8_t* trace_sat, int n_traced,
+                    const StepRule& rule, cudaStream_t s) {
   if (M <= 0) return SPASM_OK;
   if constexpr (std::is_same<R, float>::value) {
-    if (trace_cost == nullptr) {
+    if (trace_cost == nullptr && rule.is_reference()) {
       const int r = launch_schedule_tile(m, src, rows, M, k_lin, k_quad, eta, alpha, out_values, out_cost, flagged,
                                          flagged_count, s);
       if (r != -1) return r;
@@ -136,19 +137,19 @@ int launch_schedule(const Model& m, const R* src, const uint32_t* rows, int64_t 
   }
   return dispatch_model<R>(m, [&](auto e, const auto& sc) -> int {
     using E = decltype(e);
-    const size_t per = (size_t)(2 * sc.dim + E::scratch_per_thread(sc)) * sizeof(R);
+    const size_t per = (size_t)((rule.adam ? 4 : 2) * sc.dim + E::scratch_per_thread(sc)) * sizeof(R);
     const int bs = pick_block(M, per);
     const size_t smem = per * bs;
     if (trace_cost != nullptr && n_traced > 0) {
       allow_big_smem(k_schedule<E, R, true>);
       k_schedule<E, R, true><<<ceil_div(M, bs), bs, smem, s>>>(sc, src, rows, M, k_lin, k_quad, eta, alpha, eps,
                                                                out_values, out_cost, flagged, flagged_count,
-                                                               trace_cost, trace_sat, n_traced);
+                                                               trace_cost, trace_sat, n_traced, rule);
     } else {
       allow_big_smem(k_schedule<E, R, false>);
       k_schedule<E, R, false><<<ceil_div(M, bs), bs, smem, s>>>(sc, src, rows, M, k_lin, k_quad, eta, alpha, eps,
                                                                 out_values, out_cost, flagged, flagged_count,
-                                                                nullptr, nullptr, 0);
+                                                                nullptr, nullptr, 0, rule);
     }
     SPASM_CHECK_LAUNCH();
     return SPASM_OK;

@@ -201,6 +201,15 @@ class OptimizerConfig:
     p_return: int = 32
     max_restarts: int = 64
     seed: int = 0
+    # perf-mode particle update (north_star item 4; not in the reference, whose defaults
+    # these keep): "adam" scales Adam moments by the same learning-rate schedule;
+    # noise_sigma > 0 adds Gaussian noise (std = noise_sigma x bound width, Philox stream)
+    # annealed linearly to 0 over the K_lin linear steps
+    update: str = "gd"
+    adam_beta1: float = 0.9
+    adam_beta2: float = 0.999
+    adam_eps: float = 1e-8
+    noise_sigma: float = 0.0
 
     def __post_init__(self):
         if not (1 <= self.m <= self.n):
@@ -215,6 +224,24 @@ class OptimizerConfig:
             raise ValueError("p_return must be >= 1")
         if self.max_restarts < 1:
             raise ValueError("max_restarts must be >= 1")
+        if self.update not in ("gd", "adam"):
+            raise ValueError("update must be 'gd' or 'adam'")
+        if self.noise_sigma < 0:
+            raise ValueError("noise_sigma must be >= 0")
+        if self.update == "adam" and not (0 <= self.adam_beta1 < 1 and 0 <= self.adam_beta2 < 1 and self.adam_eps > 0):
+            raise ValueError("Adam needs 0 <= beta1, beta2 < 1 and eps > 0")
+
+    @property
+    def reference_update(self) -> bool:
+        """True when the particle update is the reference's clamped gradient step."""
+        return self.update == "gd" and self.noise_sigma == 0.0
+
+    def native(self, sampler: int, n_traced: int = 0):
+        """The spasm_solve_config C struct of this configuration."""
+        return nat.spasm_solve_config(self.n, self.m, self.k_lin, self.k_quad, self.eta_init, self.alpha,
+                                      self.epsilon, self.p_return, self.max_restarts, self.seed, sampler, n_traced,
+                                      1 if self.update == "adam" else 0, self.adam_beta1, self.adam_beta2,
+                                      self.adam_eps, self.noise_sigma)
 
 
 @dataclass
@@ -487,6 +514,8 @@ def solve(cost_model: CostModel, config: OptimizerConfig, *, warm_seeds=None, th
     nat.require_cuda()
     if isinstance(cost_model, NativeCostModel):
         return _solve_native(cost_model, config, warm_seeds, trace, _SAMPLERS[sampler])
+    if not config.reference_update:
+        raise ValueError("update='adam' / noise_sigma > 0 run inside the native kernels: use a native cost model")
     return _solve_generic(cost_model, config, warm_seeds, trace, _SAMPLERS[sampler])
 
 
@@ -534,8 +563,7 @@ def _solve_native(model: NativeCostModel, config: OptimizerConfig, warm_seeds, t
         else:
             warm = None
     n_traced = min(config.m, TRACE_PARTICLE_CAP) if trace else 0
-    cfg = nat.spasm_solve_config(config.n, config.m, config.k_lin, config.k_quad, config.eta_init, config.alpha,
-                                 config.epsilon, config.p_return, config.max_restarts, config.seed, sampler, n_traced)
+    cfg = config.native(sampler, n_traced)
     ws = _WS.get(model, cfg, n_warm)
     parts = np.zeros((config.p_return, D))
     costs = np.zeros(config.p_return)

@@ -90,9 +90,7 @@ class NativeShardOps:
         nat.require_cuda()
         self.model = model
         self.lib = nat.load()
-        self.cfg = nat.spasm_solve_config(config.n, config.m, config.k_lin, config.k_quad, config.eta_init,
-                                          config.alpha, config.epsilon, config.p_return, config.max_restarts,
-                                          config.seed, sampler, 0)
+        self.cfg = config.native(sampler)
         self.m = config.m
         self.p = config.p_return
         self.D = model.dimension
