@@ -145,6 +145,27 @@ __device__ __forceinline__ void tile_sphere(const ChainDesc<R>& ch, const TileFr
   c[2] = t[2] + f.o[2];
 }
 
+// Bitwise state equality across the tile. The DLS iterations below are pure functions of
+// the joint vector, so once an iteration reproduces the previous state (fixed point) or
+// the state before it (period-2 cycle) every later iteration is known exactly: the loops
+// stop there and land on the state the reference would hold after its last iteration.
+template <typename R>
+__device__ __forceinline__ bool bits_eq(R a, R b) {
+  if constexpr (sizeof(R) == 4) return __float_as_uint(a) == __float_as_uint(b);
+  else return __double_as_longlong(a) == __double_as_longlong(b);
+}
+
+// Returns true when the loop can stop; qj is then the state after iteration max_iters-1.
+template <typename R>
+__device__ __forceinline__ bool tile_settled(const Tile& tl, R& qj, R& prev1, R& prev2, int it, int max_iters) {
+  const bool fixed = __all_sync(tl.mask, bits_eq(qj, prev1));
+  const bool cycle = !fixed && it >= 1 && __all_sync(tl.mask, bits_eq(qj, prev2));
+  if (cycle && ((max_iters - 1 - it) & 1)) qj = prev1;  // odd number of steps left: other phase
+  prev2 = prev1;
+  prev1 = qj;
+  return fixed || cycle;
+}
+
 // One damped least-squares step on the tile: A = sum_j col_j col_j^T + damping I (xor
 // reduced, identical on every lane), Cholesky, dq_j = col_j . y, max|dq| <= 0.5.
 template <typename R, int NR>
@@ -175,6 +196,7 @@ __device__ bool tile_ik(const Tile& tl, const ChainDesc<R>& ch, R& qj, const R t
   const int j = tl.j;
   const bool live = j < ch.J;
   TileFrame<R> f;
+  R prev1 = qj, prev2 = qj;
   for (int it = 0; it < max_iters; ++it) {
     tile_fk(tl, ch, qj, f);
     const R pe[3] = {tp[0] - f.ee[0], tp[1] - f.ee[1], tp[2] - f.ee[2]};
@@ -191,6 +213,7 @@ __device__ bool tile_ik(const Tile& tl, const ChainDesc<R>& ch, R& qj, const R t
       const R v = qj + dq;
       qj = v < ch.lo[j] ? ch.lo[j] : (v > ch.hi[j] ? ch.hi[j] : v);
     }
+    if (tile_settled(tl, qj, prev1, prev2, it, max_iters)) break;
   }
   tile_fk(tl, ch, qj, f);
   const R pe[3] = {tp[0] - f.ee[0], tp[1] - f.ee[1], tp[2] - f.ee[2]};
@@ -200,15 +223,31 @@ __device__ bool tile_ik(const Tile& tl, const ChainDesc<R>& ch, R& qj, const R t
   return pn < R(kIkPosTol) && ye < R(kIkYawTol);
 }
 
-// _polish_tool_down for one configuration on a tile (trajopt.py:726-776)
+// _polish_tool_down for one configuration on a tile (trajopt.py:726-776). Optional
+// speculative mode (k_ik_group): `best` points at a shared slot that becomes the winning
+// tile's index once every restart has finished IK; a tile whose index `me` lost stops
+// polishing (its result is discarded, so the winner's result is unchanged).
 template <typename R>
-__device__ bool tile_polish(const Tile& tl, const ChainDesc<R>& ch, R& qj, const R tp[3], R ty) {
+__device__ bool tile_polish(const Tile& tl, const ChainDesc<R>& ch, R& qj, const R tp[3], R ty,
+                            const volatile int* best = nullptr, int me = 0,
+                            const volatile unsigned long long* cur = nullptr, unsigned long long mine = 0,
+                            bool* completed = nullptr) {
+  if (completed) *completed = false;
   const int j = tl.j;
   const bool live = j < ch.J;
   const R cos_tol = R(0.99998750002604164);  // cos(0.005)
   const R two_pi = R(6.283185307179586476925286766559);
   TileFrame<R> f;
+  R prev1 = qj, prev2 = qj;
   for (int it = 0; it < kPolishMaxIters; ++it) {
+    if (best) {  // abort once another tile is the winner or the current best candidate
+      int stop = 0;
+      if (j == 0) {
+        const int b = *best;
+        stop = (b >= 0) ? (b != me) : (cur != nullptr && *cur != mine);
+      }
+      if (__shfl_sync(tl.mask, stop, 0, kTile)) return false;
+    }
     tile_fk(tl, ch, qj, f);
     const R pe[3] = {tp[0] - f.ee[0], tp[1] - f.ee[1], tp[2] - f.ee[2]};
     const R ye = wrap_yaw(ty - yaw_of(f.Ree));
@@ -227,10 +266,12 @@ __device__ bool tile_polish(const Tile& tl, const ChainDesc<R>& ch, R& qj, const
       if (ch.full_circle[j]) v = ch.lo[j] + np_mod_pos(v - ch.lo[j], two_pi);
       qj = v < ch.lo[j] ? ch.lo[j] : (v > ch.hi[j] ? ch.hi[j] : v);
     }
+    if (tile_settled(tl, qj, prev1, prev2, it, kPolishMaxIters)) break;
   }
   tile_fk(tl, ch, qj, f);
   const R pe[3] = {tp[0] - f.ee[0], tp[1] - f.ee[1], tp[2] - f.ee[2]};
   const R pn = Math<R>::sqrt_((pe[0] * pe[0] + pe[1] * pe[1]) + pe[2] * pe[2]);
+  if (completed) *completed = true;
   return pn < R(kIkPosTol) && fabs(wrap_yaw(ty - yaw_of(f.Ree))) < R(kIkYawTol) && -f.Ree[8] > cos_tol;
 }
 

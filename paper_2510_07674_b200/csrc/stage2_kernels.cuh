@@ -65,9 +65,11 @@ __device__ __forceinline__ void lift_target(const TrajScene<R>& sc, const double
   *ty = (R)wrap_yaw<double>(yaw + (double)sc.grasp_yaw);
 }
 
-// one CTA per (draw, target) group; one 8-lane tile per seeded restart (lane = joint)
+// one CTA per (draw, target) group; one 8-lane tile per seeded restart (lane = joint), each
+// tile in its own warp (lanes 8-31 idle) so that restarts in different phases (IK vs
+// speculative polish) never share a warp and serialise on divergence
 template <typename R>
-__global__ void __launch_bounds__(256) k_ik_group(const TrajScene<R>* __restrict__ g_scene, int n_targets, int n_draws,
+__global__ void __launch_bounds__(1024) k_ik_group(const TrajScene<R>* __restrict__ g_scene, int n_targets, int n_draws,
                                                   uint64_t seed, uint64_t draw_stride, int restarts, int max_iters,
                                                   double damping, const double* __restrict__ tpos_in,
                                                   const double* __restrict__ tyaw_in, const double* __restrict__ rows,
@@ -75,7 +77,13 @@ __global__ void __launch_bounds__(256) k_ik_group(const TrajScene<R>* __restrict
   __shared__ ChainDesc<R> ch_s;
   __shared__ R s_key[32], s_score[32];
   __shared__ int s_ok[32];
-  __shared__ int s_best;
+  __shared__ int s_best, s_done;
+  __shared__ unsigned long long s_cur;  // best (approximate key, restart) among finished restarts
+  if (threadIdx.x == 0) {
+    s_best = -1;
+    s_done = 0;
+    s_cur = ~0ull;
+  }
   const TrajScene<R>& sc = *g_scene;
   {
     const int4* src = reinterpret_cast<const int4*>(&sc.ch);
@@ -88,7 +96,8 @@ __global__ void __launch_bounds__(256) k_ik_group(const TrajScene<R>* __restrict
   const int a = grp / n_targets, t = grp - a * n_targets;
   const int J = ch.J;
   const Tile tl = Tile::make();
-  const int tile = threadIdx.x >> 3;
+  const int tile = threadIdx.x >> 5;
+  const bool tile_lane = (threadIdx.x & 31) < kTile;
   R tp[3], ty;
   if (tpos_in) {
     tp[0] = (R)tpos_in[3 * t];
@@ -99,7 +108,9 @@ __global__ void __launch_bounds__(256) k_ik_group(const TrajScene<R>* __restrict
     lift_target<R>(sc, rows, D, t, tp, &ty);
   }
   R qj = R(0);
-  if (tile < restarts) {
+  bool pol_spec = true, spec_done = false;
+  R ik_q = R(0);
+  if (tile < restarts && tile_lane) {
     if (tl.j < J) {
       // seeds[t] = uniform(lower, upper, (restarts, dof)) of SeedSequence(seed, (t,)) (robot.py:255-257)
       Pcg64 g;
@@ -110,25 +121,43 @@ __global__ void __launch_bounds__(256) k_ik_group(const TrajScene<R>* __restrict
     }
     R score;
     const bool ok = tile_ik<R>(tl, ch, qj, tp, ty, max_iters, R(damping), &score);
+    const R key = (ok ? R(0) : R(1e6)) + score;
+    // speculation order: (fp32 image of the key, restart); the exact winner is s_best below
+    const unsigned long long mine = ((unsigned long long)order_key((float)key) << 32) | (unsigned)tile;
+    int last = 0, lead = 0;
     if (tl.j == 0) {
-      s_key[tile] = (ok ? R(0) : R(1e6)) + score;
+      s_key[tile] = key;
       s_score[tile] = score;
       s_ok[tile] = ok;
+      __threadfence_block();
+      lead = atomicMin(&s_cur, mine) > mine;
+      last = atomicAdd(&s_done, 1) == restarts - 1;
     }
+    last = __shfl_sync(tl.mask, last, 0, kTile);
+    lead = __shfl_sync(tl.mask, lead, 0, kTile);
+    if (last && tl.j == 0) {  // the last restart to finish picks the first minimum (np.argmin)
+      __threadfence_block();
+      int b = 0;
+      for (int r = 1; r < restarts; ++r)
+        if (((volatile R*)s_key)[r] < ((volatile R*)s_key)[b]) b = r;
+      *((volatile int*)&s_best) = b;
+    }
+    // speculative polish (lift path): the best restart finished so far starts polishing
+    // its IK result at once and stops if a better one finishes or another tile wins, so
+    // the winner's polish usually overlaps the slower restarts' IK iterations
+    ik_q = qj;
+    if (polish && lead) pol_spec = tile_polish<R>(tl, ch, qj, tp, ty, &s_best, tile, &s_cur, mine, &spec_done);
   }
   __syncthreads();
-  if (threadIdx.x == 0) {  // first minimum over restarts (np.argmin)
-    int b = 0;
-    for (int r = 1; r < restarts; ++r)
-      if (s_key[r] < s_key[b]) b = r;
-    s_best = b;
-  }
-  __syncthreads();
-  if (tile != s_best) return;
+  if (tile != s_best || !tile_lane) return;
   bool pol = true;
   R pen = R(0);
   if (polish) {
-    pol = tile_polish<R>(tl, ch, qj, tp, ty);
+    if (!spec_done) {  // the winner was not (fully) polished speculatively: polish it now
+      qj = ik_q;
+      pol_spec = tile_polish<R>(tl, ch, qj, tp, ty);
+    }
+    pol = pol_spec;
     if (score_statics && sc.n_static > 0) pen = tile_arm_worst_pen<R>(tl, ch, qj, sc.st_c, sc.st_r, sc.n_static);
   }
   if (tl.j < J) reinterpret_cast<R*>(out.sol)[(int64_t)grp * J + tl.j] = qj;

@@ -158,7 +158,7 @@ int launch_ik(const Traj& tr, int n_targets, int n_draws, uint64_t seed, uint64_
   if (n_targets <= 0) return SPASM_OK;
   SPASM_REQUIRE(restarts >= 1 && restarts <= 32, "restarts must be in [1, 32]");
   const int64_t groups = (int64_t)n_targets * n_draws;
-  const int bs = (restarts * kTile + 31) / 32 * 32;
+  const int bs = restarts * 32;  // one warp per restart tile (k_ik_group)
   const int64_t grid = groups;
   k_ik_group<R><<<(unsigned)grid, bs, 0, s>>>(tr.dev<R>(), n_targets, n_draws, seed, stride, restarts, max_iters,
                                               damping, tpos, tyaw, rows, D, polish, score_statics, out);
