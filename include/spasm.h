@@ -304,6 +304,11 @@ int spasm_solve_al(const spasm_traj* traj, int dtype, const spasm_al_config* cfg
                    const int32_t* n_active, const int32_t* lift_status, void* workspace, int64_t workspace_bytes,
                    void* best_values, spasm_al_result* result, void* stream);
 
+/* Diagnostic: per-phase cycle counters of the fp32 AL kernel (marks 0-4: inner-step phases
+ * P1-P5, 8: pick-waypoint polish, 9: re-evaluation + validate). enable 1/0; out (12
+ * doubles, optional) receives and resets the counters. */
+int spasm_al_profile(int enable, double* out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -94,8 +94,29 @@ enum : int {
   kWorst, kLr
 };
 
+// Optional phase timer (diagnostic, spasm_al_profile): thread 0 accumulates clock64()
+// deltas between consecutive marks; off unless enabled (one predicated branch per mark).
+static __device__ unsigned long long g_al_prof[12];
+static __device__ int g_al_prof_on;
+struct AlProf {
+  bool on = false;
+  long long t = 0;
+  __device__ __forceinline__ void start() {
+    on = g_al_prof_on != 0;
+    if (on) t = clock64();
+  }
+  __device__ __forceinline__ void mark(int k) {
+    if (on && threadIdx.x == 0) {
+      const long long n = clock64();
+      atomicAdd(&g_al_prof[k], (unsigned long long)(n - t));
+      t = n;
+    }
+  }
+};
+
 template <typename R>
 struct AlCtx {
+  AlProf prof;
   AlLayout L;
   TrajScene<R>* sc;
   R *x, *g, *unit, *ee, *rot, *armw, *ga, *hp, *gh, *pg, *pl, *psi, *cp, *sp, *rows, *gpose, *scr, *pgsum, *red, *scal;
@@ -132,12 +153,24 @@ struct AlCtx {
 // the unscaled slope (d value / d ca = -slope * (ca - cb)) (trajopt.py:396-413)
 template <typename R>
 __device__ __forceinline__ R pen_term(R dx, R dy, R dz, R rsum, bool quad, R* slope) {
-  const R d = Math<R>::sqrt_((dx * dx + dy * dy) + dz * dz);
-  R pen = rsum - d;
-  pen = pen > R(0) ? pen : R(0);
-  const bool live = pen > R(0) && d > R(0);
-  *slope = live ? (quad ? R(2) * pen / d : R(1) / d) : R(0);
-  return quad ? pen * pen : pen;
+  if constexpr (sizeof(R) == 4) {
+    // fp32: one MUFU.RSQ for both d and 1/d (d2 = 0 -> d = NaN -> inactive, zero slope)
+    const R d2 = (dx * dx + dy * dy) + dz * dz;
+    const R inv = rsqrtf(d2);
+    const R d = d2 * inv;
+    R pen = rsum - d;
+    const bool live = pen > R(0);
+    pen = live ? pen : R(0);
+    *slope = live ? (quad ? R(2) * pen * inv : inv) : R(0);
+    return quad ? pen * pen : pen;
+  } else {
+    const R d = Math<R>::sqrt_((dx * dx + dy * dy) + dz * dz);
+    R pen = rsum - d;
+    pen = pen > R(0) ? pen : R(0);
+    const bool live = pen > R(0) && d > R(0);
+    *slope = live ? (quad ? R(2) * pen / d : R(1) / d) : R(0);
+    return quad ? pen * pen : pen;
+  }
 }
 
 // accumulate one sphere (centre c, radius r) against fixed obstacles: statics + staged
@@ -145,7 +178,8 @@ __device__ __forceinline__ R pen_term(R dx, R dy, R dz, R rsum, bool quad, R* sl
 template <typename R>
 __device__ __forceinline__ R pens_fixed(const TrajScene<R>& sc, const R* c, R r, int f0, int f1, bool quad, R* g) {
   R v = R(0);
-  for (int o = 0; o < sc.n_static; ++o) {
+#pragma unroll 4
+  for (int o = 0; o < sc.n_static; ++o) {  // unrolled: overlaps the per-pair MUFU latencies
     const R dx = c[0] - sc.st_c[o][0], dy = c[1] - sc.st_c[o][1], dz = c[2] - sc.st_c[o][2];
     R sl;
     v += pen_term(dx, dy, dz, r + sc.st_r[o], quad, &sl);
@@ -153,10 +187,32 @@ __device__ __forceinline__ R pens_fixed(const TrajScene<R>& sc, const R* c, R r,
     g[1] -= sl * dy;
     g[2] -= sl * dz;
   }
+#pragma unroll 4
   for (int o = f0; o < f1; ++o) {
     const R dx = c[0] - sc.staged[o][0], dy = c[1] - sc.staged[o][1], dz = c[2] - sc.staged[o][2];
     R sl;
     v += pen_term(dx, dy, dz, r + sc.br[o], quad, &sl);
+    g[0] -= sl * dx;
+    g[1] -= sl * dy;
+    g[2] -= sl * dz;
+  }
+  return v;
+}
+
+// The same for one lane of an 8-lane tile: obstacles o = lane, lane + 8, ... of the
+// combined list (statics, then staged spheres [f0, f1)); the caller tile-sums the results.
+template <typename R>
+__device__ __forceinline__ R pens_fixed_lane(const TrajScene<R>& sc, const R* c, R r, int f0, int f1, bool quad,
+                                             int lane, R* g) {
+  R v = R(0);
+  const int ns = sc.n_static, nfix = ns + (f1 - f0);
+#pragma unroll 2
+  for (int o = lane; o < nfix; o += kTile) {
+    const R* oc = o < ns ? sc.st_c[o] : sc.staged[f0 + o - ns];
+    const R orad = o < ns ? sc.st_r[o] : sc.br[f0 + o - ns];
+    const R dx = c[0] - oc[0], dy = c[1] - oc[1], dz = c[2] - oc[2];
+    R sl;
+    v += pen_term(dx, dy, dz, r + orad, quad, &sl);
     g[0] -= sl * dx;
     g[1] -= sl * dy;
     g[2] -= sl * dz;
@@ -260,6 +316,7 @@ __device__ void al_eval(AlCtx<R>& C, const typename TwinSceneOf<R, KIND>::type& 
     }
   }
   __syncthreads();
+  C.prof.mark(0);
 
   // ---------------- P2: aux = placed poses + placement twin; tiles = fixed obstacles ----
   if (is_aux) {
@@ -300,10 +357,18 @@ __device__ void al_eval(AlCtx<R>& C, const typename TwinSceneOf<R, KIND>::type& 
       }
     }
   } else if (is_wp) {
-    if (j < J) {
-      for (int s = ch.link_start[j]; s < ch.link_start[j + 1]; ++s) {
-        R gg[3] = {R(0), R(0), R(0)};
-        carm += pens_fixed(sc, C.armw + (w * S + s) * 3, ch.arm_r[s], f0, f1, quad, gg);
+    // every sphere of the waypoint against the fixed obstacles, the obstacle list split over
+    // the tile's 8 lanes and tile-summed (the per-lane sphere loop left one lane with all
+    // the held-block pairs on top of its link's spheres)
+    for (int s = 0; s < S; ++s) {
+      R gg[3] = {R(0), R(0), R(0)};
+      R v = pens_fixed_lane(sc, C.armw + (w * S + s) * 3, ch.arm_r[s], f0, f1, quad, j, gg);
+      v = tl.sum(v);
+      gg[0] = tl.sum(gg[0]);
+      gg[1] = tl.sum(gg[1]);
+      gg[2] = tl.sum(gg[2]);
+      if (j == 0) {
+        carm += v;
         R* ga = C.ga + (w * S + s) * 3;
         ga[0] = gg[0];
         ga[1] = gg[1];
@@ -311,17 +376,25 @@ __device__ void al_eval(AlCtx<R>& C, const typename TwinSceneOf<R, KIND>::type& 
       }
     }
     if (interior) {
-      for (int s = j; s < nh; s += kTile) {
+      for (int s = 0; s < nh; ++s) {
         R gg[3] = {R(0), R(0), R(0)};
-        cblk += pens_fixed(sc, C.hp + (w * SBn + s) * 3, sc.br[h0 + s], f0, f1, quad, gg);
-        R* gh = C.gh + (w * SBn + s) * 3;
-        gh[0] = gg[0];
-        gh[1] = gg[1];
-        gh[2] = gg[2];
+        R v = pens_fixed_lane(sc, C.hp + (w * SBn + s) * 3, sc.br[h0 + s], f0, f1, quad, j, gg);
+        v = tl.sum(v);
+        gg[0] = tl.sum(gg[0]);
+        gg[1] = tl.sum(gg[1]);
+        gg[2] = tl.sum(gg[2]);
+        if (j == 0) {
+          cblk += v;
+          R* gh = C.gh + (w * SBn + s) * 3;
+          gh[0] = gg[0];
+          gh[1] = gg[1];
+          gh[2] = gg[2];
+        }
       }
     }
   }
   __syncthreads();
+  C.prof.mark(1);
 
   // ---------------- P3: placed blocks, placed-pose partials, J^T products ------------------
   st.garm = R(0);
@@ -455,6 +528,7 @@ __device__ void al_eval(AlCtx<R>& C, const typename TwinSceneOf<R, KIND>::type& 
     }
   }
   __syncthreads();
+  C.prof.mark(2);
 
   // ---------------- P4: totals, multiplier scales; aux reduces placed partials ----------
   if (tid == 0) {
@@ -488,6 +562,7 @@ __device__ void al_eval(AlCtx<R>& C, const typename TwinSceneOf<R, KIND>::type& 
     }
   }
   __syncthreads();
+  C.prof.mark(3);
 
   // ---------------- P5: gradient assembly (lane k = joint k) + optional update -----------
   if (want_grad && is_wp && j < J) {
@@ -539,6 +614,7 @@ __device__ void al_eval(AlCtx<R>& C, const typename TwinSceneOf<R, KIND>::type& 
     }
   }
   __syncthreads();
+  C.prof.mark(4);
 }
 
 // ---------------------------------------------------------------------------------------
@@ -790,6 +866,7 @@ __global__ void __launch_bounds__(kMaxAlThreads) k_solve_al(const TrajScene<R>* 
     C.flags[0] = 0;
   }
   __syncthreads();
+  C.prof.start();
   const R denom = R(prm.inner_steps - 1 > 1 ? prm.inner_steps - 1 : 1);
   int first = -1, done = 0;
   for (int outer = 0; outer < prm.outer_iters; ++outer) {
@@ -811,8 +888,10 @@ __global__ void __launch_bounds__(kMaxAlThreads) k_solve_al(const TrajScene<R>* 
       if (tl.j < J) C.x[w0 * kXS + tl.j] = qj;
     }
     __syncthreads();
+    C.prof.mark(8);  // pick-waypoint polish (+ the last inner step's tail)
     al_eval<R, KIND, SPB>(C, tw, prm, false, prm.place_mode == 1, false, R(0));
     al_validate<R, KIND, SPB>(C, tw, prm);
+    C.prof.mark(9);  // re-evaluation + validate (eval marks fold into 0-4)
     if (tid == 0) {
       const int64_t o = (int64_t)outer * P + p;
       const R mu = C.scal[kMu];

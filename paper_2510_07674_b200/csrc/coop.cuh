@@ -156,10 +156,16 @@ __device__ __forceinline__ bool bits_eq(R a, R b) {
 }
 
 // Returns true when the loop can stop; qj is then the state after iteration max_iters-1.
+// (checked every 8th iteration: the vote is not free, and the states are kept every step)
 template <typename R>
 __device__ __forceinline__ bool tile_settled(const Tile& tl, R& qj, R& prev1, R& prev2, int it, int max_iters) {
+  if ((it & 7) != 7) {
+    prev2 = prev1;
+    prev1 = qj;
+    return false;
+  }
   const bool fixed = __all_sync(tl.mask, bits_eq(qj, prev1));
-  const bool cycle = !fixed && it >= 1 && __all_sync(tl.mask, bits_eq(qj, prev2));
+  const bool cycle = !fixed && __all_sync(tl.mask, bits_eq(qj, prev2));
   if (cycle && ((max_iters - 1 - it) & 1)) qj = prev1;  // odd number of steps left: other phase
   prev2 = prev1;
   prev1 = qj;

@@ -52,7 +52,7 @@ __device__ R twin_tetris_warp(const TetrisScene<R>& sc, const R* rows, R* grad, 
   __syncwarp();
   R cost = R(0);
   const int npairs = n * (n - 1) / 2;
-  const int items = npairs + (sc.n_static > 0 ? n : 0);
+  const int items = npairs + (sc.n_static > 0 ? sc.body_start[n] : 0);  // + one item per sphere vs statics
   for (int it = lane; it < items; it += 32) {
     if (it < npairs) {
       int i = 0, rem = it;
@@ -94,11 +94,13 @@ __device__ R twin_tetris_warp(const TetrisScene<R>& sc, const R* rows, R* grad, 
         my[4 * j + 3] -= wneg * gyj;
       }
     } else {
-      const int i = it - npairs;
+      const int a = it - npairs;  // movable sphere a of body i vs every static
+      int i = 0;
+      while (sc.body_start[i + 1] <= a) ++i;
       const R ci = cs[2 * i], si = cs[2 * i + 1];
       const R pix = rows[4 * i], piy = rows[4 * i + 1], piz = rows[4 * i + 2];
       R gx = R(0), gy = R(0), gz = R(0), gw = R(0);
-      for (int a = sc.body_start[i]; a < sc.body_start[i + 1]; ++a) {
+      {
         const R rx = ci * sc.lx[a] - si * sc.ly[a], ry = si * sc.lx[a] + ci * sc.ly[a];
         const R wax = pix + rx, way = piy + ry, waz = piz + sc.lz[a];
         R gax = R(0), gay = R(0), gaz = R(0);

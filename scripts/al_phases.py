@@ -1,0 +1,31 @@
+"""Per-phase cycle breakdown of the fp32 AL kernel on a pipeline workload (diagnostic).
+Usage: python scripts/al_phases.py [scene] [solves]"""
+import sys
+
+import numpy as np
+
+sys.path.insert(0, ".")
+from paper_2510_07674_b200 import _native as nat  # noqa: E402
+from paper_2510_07674_b200.bench_api import solve_scene  # noqa: E402
+from paper_2510_07674_b200.problems import as_cost_model, load_scene  # noqa: E402
+
+scene_name = sys.argv[1] if len(sys.argv) > 1 else "tower3c"
+solves = int(sys.argv[2]) if len(sys.argv) > 2 else 5
+scene = load_scene(scene_name)
+model = as_cost_model(scene.problem, precision="fp32")
+lib = nat.load()
+solve_scene(scene, seed=99, model=model)
+out = np.zeros(12)
+lib.spasm_al_profile(1, None)
+lib.spasm_al_profile(1, out.ctypes.data)  # reset
+outers = 0
+for s in range(solves):
+    sol = solve_scene(scene, seed=s, model=model)
+    outers += sol.stats.get("stage2_outers", 0)
+lib.spasm_al_profile(0, out.ctypes.data)
+names = {0: "P1 FK/spheres/leg/start", 1: "P2 fixed obstacles + twin", 2: "P3 placed blocks + J^T",
+         3: "P4 totals/scales", 4: "P5 assemble + step", 8: "pick polish", 9: "re-eval + validate"}
+tot = out.sum()
+print(f"scene {scene_name}: {solves} solves, {outers} outers; cycles by phase (thread 0, summed over CTAs):")
+for k, n in names.items():
+    print(f"  {n:28s} {out[k] / tot * 100:6.1f}%  {out[k] / max(1, outers):14.0f} cycles/outer")
