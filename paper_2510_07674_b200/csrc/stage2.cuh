@@ -166,7 +166,9 @@ __device__ __forceinline__ R wrap_yaw(R a) {
 // np.mod(a, m) for m > 0 (npy_divmod: result carries the divisor's sign)
 template <typename R>
 __device__ __forceinline__ R np_mod_pos(R a, R m) {
-  R r = fmod(a, m);
+  // a in [-m, 2m) (a clamped joint plus a step <= 0.5 rad): fmod is a - m or a, and a - m
+  // is exact there (Sterbenz), so the branch below gives fmod's bits without its loop
+  R r = (a >= -m && a < R(2) * m) ? (a >= m ? a - m : a) : fmod(a, m);
   if (r != R(0)) {
     if (r < R(0)) r += m;
   } else {
@@ -197,35 +199,69 @@ __device__ __forceinline__ void cross3(const R* a, const R* b, R* c) {
 // Solve (A) y = e for SPD A (N x N, row-major) by Cholesky in registers.
 template <typename R, int N>
 __device__ __forceinline__ void chol_solve(R* A, const R* e, R* y) {
+  if constexpr (sizeof(R) == 4) {
+    // fp32 (perf path): one MUFU.RSQ per pivot, multiplications instead of divisions
+    R inv[N];
 #pragma unroll
-  for (int j = 0; j < N; ++j) {
-    R d = A[j * N + j];
+    for (int j = 0; j < N; ++j) {
+      R d = A[j * N + j];
 #pragma unroll
-    for (int k = 0; k < j; ++k) d -= A[j * N + k] * A[j * N + k];
-    d = Math<R>::sqrt_(d);
-    A[j * N + j] = d;
+      for (int k = 0; k < j; ++k) d -= A[j * N + k] * A[j * N + k];
+      inv[j] = rsqrtf(d);
 #pragma unroll
-    for (int i = j + 1; i < N; ++i) {
-      R s = A[i * N + j];
+      for (int i = j + 1; i < N; ++i) {
+        R s = A[i * N + j];
 #pragma unroll
-      for (int k = 0; k < j; ++k) s -= A[i * N + k] * A[j * N + k];
-      A[i * N + j] = s / d;
+        for (int k = 0; k < j; ++k) s -= A[i * N + k] * A[j * N + k];
+        A[i * N + j] = s * inv[j];
+      }
     }
-  }
-  R z[N];
+    R z[N];
 #pragma unroll
-  for (int i = 0; i < N; ++i) {
-    R s = e[i];
+    for (int i = 0; i < N; ++i) {
+      R s = e[i];
 #pragma unroll
-    for (int k = 0; k < i; ++k) s -= A[i * N + k] * z[k];
-    z[i] = s / A[i * N + i];
-  }
+      for (int k = 0; k < i; ++k) s -= A[i * N + k] * z[k];
+      z[i] = s * inv[i];
+    }
 #pragma unroll
-  for (int i = N - 1; i >= 0; --i) {
-    R s = z[i];
+    for (int i = N - 1; i >= 0; --i) {
+      R s = z[i];
 #pragma unroll
-    for (int k = i + 1; k < N; ++k) s -= A[k * N + i] * y[k];
-    y[i] = s / A[i * N + i];
+      for (int k = i + 1; k < N; ++k) s -= A[k * N + i] * y[k];
+      y[i] = s * inv[i];
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < N; ++j) {
+      R d = A[j * N + j];
+#pragma unroll
+      for (int k = 0; k < j; ++k) d -= A[j * N + k] * A[j * N + k];
+      d = Math<R>::sqrt_(d);
+      A[j * N + j] = d;
+#pragma unroll
+      for (int i = j + 1; i < N; ++i) {
+        R s = A[i * N + j];
+#pragma unroll
+        for (int k = 0; k < j; ++k) s -= A[i * N + k] * A[j * N + k];
+        A[i * N + j] = s / d;
+      }
+    }
+    R z[N];
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      R s = e[i];
+#pragma unroll
+      for (int k = 0; k < i; ++k) s -= A[i * N + k] * z[k];
+      z[i] = s / A[i * N + i];
+    }
+#pragma unroll
+    for (int i = N - 1; i >= 0; --i) {
+      R s = z[i];
+#pragma unroll
+      for (int k = i + 1; k < N; ++k) s -= A[k * N + i] * y[k];
+      y[i] = s / A[i * N + i];
+    }
   }
 }
 
