@@ -234,9 +234,10 @@ static int solve_impl(Model& m, const spasm_solve_config& cfg, const double* war
     total_steps += per_restart;
     {  // kernels this restart launched: sample_eval, 2 sorts (3 kernels per 8-bit pass),
        // schedule, [trace ids], sat keys, gather, re-check evaluate, re-check copy
-      const int passes = (int)sizeof(R);
-      launches += 1 + (cfg.n > 1 ? 3 * passes : 0) + 1 + (tr && trace_ids ? 1 : 0) + 1 +
-                  (cfg.m > 1 ? 3 * passes : 0) + 3;
+      const int bits = 8 * (int)sizeof(R);
+      const int sample = (sizeof(R) == 4 && m.tile_ok && stage1_tile_mode() != 0) ? 2 : 1;  // k_sample + k_keys_tile
+      launches += sample + radix_sort_launches(cfg.n, bits) + 1 + (tr && trace_ids ? 1 : 0) + 1 +
+                  radix_sort_launches(cfg.m, bits) + 3;
     }
     total_flagged += (int)hc[1];
     const int n_sat = (int)hc[0];

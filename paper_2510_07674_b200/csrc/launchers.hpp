@@ -5,6 +5,7 @@
 #pragma once
 #include "model.hpp"
 #include "rng.cuh"
+#include "sort.cuh"
 
 // Binds R to the arithmetic type selected by a SPASM_F32 / SPASM_F64 dtype argument.
 #define SPASM_DTYPE_SWITCH(dtype, ...)                          \
@@ -23,6 +24,7 @@
 
 namespace spasm {
 
+int stage1_tile_mode();  // spasm_set_option("stage1_tile")
 void seedseq_pcg64(uint64_t seed, const uint64_t* spawn_key, int n_spawn, uint64_t out[4]);
 
 // ---- launchers (explicitly instantiated in stage1_f32.cu / stage1_f64.cu) ----------

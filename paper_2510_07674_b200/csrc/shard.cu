@@ -168,7 +168,10 @@ static int shard_select_impl(const Model& m, const spasm_solve_config& cfg, int 
   k_elite_records<K><<<ceil_div(cfg.m, 256), 256, 0, s>>>(in1 ? k1 : k0, in1 ? i1 : i0, n_local, cfg.m,
                                                           reinterpret_cast<ulonglong2*>(elite));
   SPASM_CHECK_LAUNCH();
-  if (launches) *launches = (n_local > 0 ? 1 : 0) + (n_local > 1 ? 3 * (int)sizeof(R) : 0) + 1;
+  if (launches) {
+    const int sample = (sizeof(R) == 4 && m.tile_ok && stage1_tile_mode() != 0) ? 2 : 1;
+    *launches = (n_local > 0 ? sample : 0) + radix_sort_launches(n_local, 8 * (int)sizeof(R)) + 1;
+  }
   return SPASM_OK;
 }
 
@@ -219,7 +222,7 @@ static int shard_descend_impl(const Model& m, const spasm_solve_config& cfg, int
   k_cand_recheck<R><<<ceil_div(cfg.p_return, 128), 128, 0, s>>>(recheck, cfg.p_return, D, cand);
   SPASM_CHECK_LAUNCH();
   if (launches) {
-    const int ps = 3 * (int)sizeof(R);
+    const int ps = radix_sort_launches(ml, 8 * (int)sizeof(R));
     *launches = 1 + (ml > 0 ? 3 : 0) + (ml > 1 ? ps : 0) + 3;
   }
   return SPASM_OK;
