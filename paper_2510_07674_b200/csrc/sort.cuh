@@ -138,8 +138,8 @@ __global__ void __launch_bounds__(kSortThreads) k_radix_scatter(const K* __restr
 // Small batches (n <= kSortCtaMax): every pass in ONE CTA of 1024 threads, chunks of 1024
 // keys scattered in order (match_any ranks + per-warp digit offsets), so the sort stays
 // stable and needs one launch instead of 3 per pass (the satisfying-particle ordering of
-// particle_opt.py:363 runs on m <= 16k keys every restart).
-constexpr int kSortCtaMax = 16384;
+// particle_opt.py:363 runs on m <= 8k keys every restart; above 8k the multi-CTA passes win).
+constexpr int kSortCtaMax = 8192;
 
 template <typename K>
 __global__ void __launch_bounds__(1024) k_radix_sort_cta(K* __restrict__ ka, uint32_t* __restrict__ va,
