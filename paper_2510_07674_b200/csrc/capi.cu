@@ -522,6 +522,31 @@ int spasm_tower_model_create(spasm_model** out, int n_blocks, double side, doubl
                     obstacle_radii, w_stability, w_height, w_collision, free_yaw, m->bounds, D);
   fill_tower<double>(m->wd, n_blocks, side, footprint_halfwidth, height_targets, n_obstacles, obstacle_centers,
                      obstacle_radii, w_stability, w_height, w_collision, free_yaw, m->bounds, D);
+  // fp32 tower tile kernel (stage1_tower_tile.cuh): fixed yaw, <= kTowerTileMaxBlocks cubes
+  m->tower_tile_ok = !free_yaw && n_blocks >= 2 && n_blocks <= kTowerTileMaxBlocks && n_obstacles <= kMaxObstacles;
+  if (m->tower_tile_ok) {
+    TowerTileScene& t = m->tower_tile;
+    std::memset(&t, 0, sizeof(t));
+    t.n = n_blocks;
+    t.n_obs = n_obstacles;
+    t.side = m->wf.side;
+    t.half = m->wf.half;
+    t.radius = m->wf.radius;
+    for (int i = 0; i < n_blocks; ++i) t.target[i] = m->wf.target[i];
+    for (int o = 0; o < n_obstacles; ++o) {
+      t.ox[o] = m->wf.ox[o];
+      t.oy[o] = m->wf.oy[o];
+      t.oz[o] = m->wf.oz[o];
+      t.orad[o] = m->wf.orad[o];
+    }
+    t.w_s = m->wf.w_s;
+    t.w_h = m->wf.w_h;
+    t.w_c = m->wf.w_c;
+    for (int d = 0; d < D; ++d) {
+      t.lower[d] = m->wf.lower[d];
+      t.upper[d] = m->wf.upper[d];
+    }
+  }
   *out = m;
   return SPASM_OK;
 }

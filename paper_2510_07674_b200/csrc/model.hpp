@@ -16,6 +16,8 @@ struct Model {
   // fp32 tile-kernel scene, valid when tile_ok (stage1_tile.cuh)
   TetrisTileScene tile;
   bool tile_ok = false;
+  TowerTileScene tower_tile;  // valid when tower_tile_ok (stage1_tower_tile.cuh)
+  bool tower_tile_ok = false;
   // double-precision bounds for the bit-exact sampler (numpy draws in float64)
   Bounds64 bounds;
   // pinned staging for solve results (grown on demand, never inside a kernel sequence)

@@ -85,6 +85,18 @@ struct TetrisTileScene {
   float lower[kTileMaxBodies * 3], upper[kTileMaxBodies * 3];
 };
 
+// fp32 tile-kernel scene for the tower scenes (stage1_tower_tile.cuh): fixed yaw, at most
+// kTowerTileMaxBlocks cubes, obstacles split over the lanes from a shared-memory copy.
+constexpr int kTowerTileMaxBlocks = 8;
+struct TowerTileScene {
+  int n, n_obs;
+  float side, half, radius;
+  float target[kTowerTileMaxBlocks];
+  float ox[kMaxObstacles], oy[kMaxObstacles], oz[kMaxObstacles], orad[kMaxObstacles];
+  float w_s, w_h, w_c;
+  float lower[kTowerTileMaxBlocks * 3], upper[kTowerTileMaxBlocks * 3];
+};
+
 // Perf-mode particle update (north_star item 4; not in the reference). The default
 // (adam = 0, noise = 0) is the reference's clamped gradient step (particle_opt.py:214-228)
 // and every parity path uses it. adam: Adam moments with bias correction, scaled by the

@@ -17,6 +17,11 @@ int launch_schedule_tile(const Model& m, const float* src, const uint32_t* rows,
                          double eta, double alpha, float* out_values, float* out_cost, uint8_t* flagged,
                          unsigned int* flagged_count, cudaStream_t s);
 
+// fp32 tower tile schedule (stage1towertile_f32.cu); returns -1 when not applicable.
+int launch_schedule_tower_tile(const Model& m, const float* src, const uint32_t* rows, int64_t M, int k_lin,
+                               int k_quad, double eta, double alpha, float* out_values, float* out_cost,
+                               uint8_t* flagged, unsigned int* flagged_count, cudaStream_t s);
+
 // fp32 tetris tile sample + evaluate (stage1tile_f32.cu); returns -1 when not applicable.
 int launch_sample_eval_tile(const Model& m, const Pcg64State& st, int64_t row_offset, int64_t rows_n,
                             const double* warm, int64_t n_warm, int use_philox, uint64_t seed, uint32_t restart,
@@ -130,8 +135,11 @@ int launch_schedule(const Model& m, const R* src, const uint32_t* rows, int64_t 
   if (M <= 0) return SPASM_OK;
   if constexpr (std::is_same<R, float>::value) {
     if (trace_cost == nullptr && rule.is_reference()) {
-      const int r = launch_schedule_tile(m, src, rows, M, k_lin, k_quad, eta, alpha, out_values, out_cost, flagged,
-                                         flagged_count, s);
+      int r = launch_schedule_tile(m, src, rows, M, k_lin, k_quad, eta, alpha, out_values, out_cost, flagged,
+                                   flagged_count, s);
+      if (r != -1) return r;
+      r = launch_schedule_tower_tile(m, src, rows, M, k_lin, k_quad, eta, alpha, out_values, out_cost, flagged,
+                                     flagged_count, s);
       if (r != -1) return r;
     }
   }

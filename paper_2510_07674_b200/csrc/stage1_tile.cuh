@@ -289,9 +289,8 @@ __device__ __forceinline__ float tile_eval(const TetrisTileScene& sc, const type
 }
 
 // One clamped step with the NaN freeze (particle_opt.py:214-228).
-template <int D>
-__device__ __forceinline__ void tile_step(const TetrisTileScene& sc, float (&x)[D], const float (&g)[D], float rate,
-                                          bool& bad) {
+template <int D, class SC>
+__device__ __forceinline__ void tile_step(const SC& sc, float (&x)[D], const float (&g)[D], float rate, bool& bad) {
   bool b = false;
 #pragma unroll
   for (int d = 0; d < D; ++d) b |= !isfinite(g[d]);

@@ -1,5 +1,5 @@
 """fp32 tetris tile kernel (stage1_tile.cuh) against the fp64 oracle and the generic
-fp32 kernel (4 lanes per particle).
+fp32 kernel (4 lanes per particle), tetris and tower scenes (stage1_tower_tile.cuh).
 
 Tolerances (north_star: per-particle costs and gradients within rtol 1e-4 in fp32):
   * 0 steps: the kernel's final QUADRATIC cost vs the oracle on the same fp32-rounded rows,
@@ -23,7 +23,7 @@ from paper_2510_07674_b200.problems import as_cost_model, load_scene
 
 pytestmark = pytest.mark.gpu
 
-SCENES = ["tetris5", "tetris8", "single1"]
+SCENES = ["tetris5", "tetris8", "single1", "tower4", "tower3c", "tower6r"]
 VARIANTS = [4]
 
 
