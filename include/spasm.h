@@ -305,8 +305,9 @@ int spasm_solve_al(const spasm_traj* traj, int dtype, const spasm_al_config* cfg
                    void* best_values, spasm_al_result* result, void* stream);
 
 /* Diagnostic: per-phase cycle counters of the fp32 AL kernel (marks 0-4: inner-step phases
- * P1-P5, 8: pick-waypoint polish, 9: re-evaluation + validate). enable 1/0; out (12
- * doubles, optional) receives and resets the counters. */
+ * P1-P5, 8: pick-waypoint polish, 9: re-evaluation + validate; 12-19 / 20-27: when thread
+ * 0 / the aux warp reached each phase's barrier). enable 1/0; out (28 doubles, optional)
+ * receives and resets the counters. */
 int spasm_al_profile(int enable, double* out);
 
 #ifdef __cplusplus

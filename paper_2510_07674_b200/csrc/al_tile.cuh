@@ -97,6 +97,7 @@ enum : int {
 // Optional phase timer (diagnostic, spasm_al_profile): thread 0 accumulates clock64()
 // deltas between consecutive marks; off unless enabled (one predicated branch per mark).
 static __device__ unsigned long long g_al_prof[12];
+static __device__ unsigned long long g_al_arrive[2][8];  // [tile thread 0 | aux lane 0][phase]
 static __device__ int g_al_prof_on;
 struct AlProf {
   bool on = false;
@@ -105,10 +106,16 @@ struct AlProf {
     on = g_al_prof_on != 0;
     if (on) t = clock64();
   }
+  // before a phase-ending barrier: how long this thread's own work in the phase took
+  __device__ __forceinline__ void arrive(int k, int aux_tid) {
+    if (on && (threadIdx.x == 0 || threadIdx.x == aux_tid))
+      atomicAdd(&g_al_arrive[threadIdx.x == 0 ? 0 : 1][k], (unsigned long long)(clock64() - t));
+  }
+  // after the barrier: phase time (slowest warp) as seen by thread 0
   __device__ __forceinline__ void mark(int k) {
-    if (on && threadIdx.x == 0) {
+    if (on) {
       const long long n = clock64();
-      atomicAdd(&g_al_prof[k], (unsigned long long)(n - t));
+      if (threadIdx.x == 0) atomicAdd(&g_al_prof[k], (unsigned long long)(n - t));
       t = n;
     }
   }
@@ -315,6 +322,7 @@ __device__ void al_eval(AlCtx<R>& C, const typename TwinSceneOf<R, KIND>::type& 
                             st.dy0 * st.dy0);
     }
   }
+  C.prof.arrive(0, C.L.NW);
   __syncthreads();
   C.prof.mark(0);
 
@@ -393,6 +401,7 @@ __device__ void al_eval(AlCtx<R>& C, const typename TwinSceneOf<R, KIND>::type& 
       }
     }
   }
+  C.prof.arrive(1, C.L.NW);
   __syncthreads();
   C.prof.mark(1);
 
@@ -527,6 +536,7 @@ __device__ void al_eval(AlCtx<R>& C, const typename TwinSceneOf<R, KIND>::type& 
       C.red[4 * (tid >> 5) + 2] = cblk;
     }
   }
+  C.prof.arrive(2, C.L.NW);
   __syncthreads();
   C.prof.mark(2);
 
@@ -561,6 +571,7 @@ __device__ void al_eval(AlCtx<R>& C, const typename TwinSceneOf<R, KIND>::type& 
       C.pgsum[it] = s;
     }
   }
+  C.prof.arrive(3, C.L.NW);
   __syncthreads();
   C.prof.mark(3);
 
@@ -613,6 +624,7 @@ __device__ void al_eval(AlCtx<R>& C, const typename TwinSceneOf<R, KIND>::type& 
       C.g[w * kXS + j] = gq;
     }
   }
+  C.prof.arrive(4, C.L.NW);
   __syncthreads();
   C.prof.mark(4);
 }

@@ -9,12 +9,18 @@
 extern "C" int spasm_al_profile(int enable, double* out) {
   using namespace spasm;
   SPASM_CUDA_TRY(cudaMemcpyToSymbol(g_al_prof_on, &enable, sizeof(int)));
-  if (out) {
-    unsigned long long h[12];
+  if (out) {  // out[0..11] phase times, out[12..19] tile arrivals, out[20..27] aux arrivals
+    unsigned long long h[12], a[2][8];
     SPASM_CUDA_TRY(cudaMemcpyFromSymbol(h, g_al_prof, sizeof(h)));
+    SPASM_CUDA_TRY(cudaMemcpyFromSymbol(a, g_al_arrive, sizeof(a)));
     for (int k = 0; k < 12; ++k) out[k] = (double)h[k];
-    const unsigned long long z[12] = {0};
+    for (int k = 0; k < 8; ++k) {
+      out[12 + k] = (double)a[0][k];
+      out[20 + k] = (double)a[1][k];
+    }
+    const unsigned long long z[12] = {0}, za[2][8] = {{0}};
     SPASM_CUDA_TRY(cudaMemcpyToSymbol(g_al_prof, z, sizeof(z)));
+    SPASM_CUDA_TRY(cudaMemcpyToSymbol(g_al_arrive, za, sizeof(za)));
   }
   return SPASM_OK;
 }

@@ -15,7 +15,7 @@ scene = load_scene(scene_name)
 model = as_cost_model(scene.problem, precision="fp32")
 lib = nat.load()
 solve_scene(scene, seed=99, model=model)
-out = np.zeros(12)
+out = np.zeros(28)
 lib.spasm_al_profile(1, None)
 lib.spasm_al_profile(1, out.ctypes.data)  # reset
 outers = 0
@@ -27,5 +27,9 @@ names = {0: "P1 FK/spheres/leg/start", 1: "P2 fixed obstacles + twin", 2: "P3 pl
          3: "P4 totals/scales", 4: "P5 assemble + step", 8: "pick polish", 9: "re-eval + validate"}
 tot = out.sum()
 print(f"scene {scene_name}: {solves} solves, {outers} outers; cycles by phase (thread 0, summed over CTAs):")
+tot = out[:12].sum()
 for k, n in names.items():
-    print(f"  {n:28s} {out[k] / tot * 100:6.1f}%  {out[k] / max(1, outers):14.0f} cycles/outer")
+    line = f"  {n:28s} {out[k] / tot * 100:6.1f}%  {out[k] / max(1, outers):14.0f} cycles/outer"
+    if k < 5:
+        line += f"   own work: tile t0 {out[12 + k] / max(1, outers):12.0f}  aux {out[20 + k] / max(1, outers):12.0f}"
+    print(line)
