@@ -39,7 +39,7 @@ constexpr int kXS = 8;  // row stride of x / g / unit in shared memory ([w][join
 
 struct AlLayout {
   int W, NW, nthreads, nwarps, J, B, T, S, SB, NB;
-  int scene, x, g, unit, ee, rot, armw, ga, hp, gh, pg, pl, seg, rows, gpose, scr, pgsum, red, scal, flags;
+  int scene, twin, x, g, unit, ee, rot, armw, ga, hp, gh, pg, pl, seg, rows, gpose, scr, pgsum, red, scal, flags;
   int total;
 };
 
@@ -65,6 +65,9 @@ __host__ __device__ inline AlLayout al_layout(int B, int T, int J, int S, int SB
     return o;
   };
   L.scene = take((int)sizeof(TrajScene<R>));
+  // the placement twin's tables: the aux warp's lanes index them with different obstacle /
+  // sphere numbers, which a kernel-parameter (constant bank) copy serialises per address
+  L.twin = take((int)(sizeof(TetrisScene<R>) > sizeof(TowerScene<R>) ? sizeof(TetrisScene<R>) : sizeof(TowerScene<R>)));
   L.x = take(W * kXS * r);
   L.g = take(W * kXS * r);
   L.unit = take(W * kXS * r);
@@ -352,7 +355,9 @@ __device__ void al_eval(AlCtx<R>& C, const typename TwinSceneOf<R, KIND>::type& 
         }
       }
       __syncwarp();
+      if (C.prof.on && lane == 0) atomicAdd(&g_al_arrive[1][5], (unsigned long long)(clock64() - C.prof.t));
       R cpl = twin_warp<R, KIND, SPB>(tw, C.rows, C.gpose, C.scr, lane, want_grad, pquad);
+      if (C.prof.on && lane == 0) atomicAdd(&g_al_arrive[1][6], (unsigned long long)(clock64() - C.prof.t));
       if (lane == 0) {
         if (sc.anchor) {
           for (int bb = 0; bb < B; ++bb) {
@@ -757,6 +762,17 @@ __device__ void al_load(AlCtx<R>& C, const TrajScene<R>* g_scene, const R* value
   __syncthreads();
 }
 
+// copy the kernel-parameter twin scene into shared memory (see AlLayout::twin)
+template <typename TW>
+__device__ const TW& twin_smem(unsigned char* smem, const AlLayout& L, const TW& tw) {
+  TW* dst = reinterpret_cast<TW*>(smem + L.twin);
+  const int* src = reinterpret_cast<const int*>(&tw);
+  int* d = reinterpret_cast<int*>(dst);
+  for (int i = threadIdx.x; i < (int)(sizeof(TW) / sizeof(int)); i += blockDim.x) d[i] = src[i];
+  __syncthreads();
+  return *dst;
+}
+
 template <typename R>
 __device__ void al_store_x(const AlCtx<R>& C, R* dst) {
   const int W = C.L.W, J = C.L.J;
@@ -782,6 +798,7 @@ __global__ void __launch_bounds__(kMaxAlThreads) k_al_eval(const TrajScene<R>* _
   C.bind(smem, L);
   const int64_t p = blockIdx.x;
   al_load(C, g_scene, values, p);
+  const auto& tws = twin_smem(smem, L, tw);
   if (threadIdx.x == 0) {
     C.scal[kLam0] = lam ? lam[3 * p] : R(0);
     C.scal[kLam1] = lam ? lam[3 * p + 1] : R(0);
@@ -789,7 +806,7 @@ __global__ void __launch_bounds__(kMaxAlThreads) k_al_eval(const TrajScene<R>* _
     C.scal[kMu] = mu ? mu[p] : R(0);
   }
   __syncthreads();
-  al_eval<R, KIND, SPB>(C, tw, prm, mode == 1, place_mode == 1, want_grad != 0, R(0));
+  al_eval<R, KIND, SPB>(C, tws, prm, mode == 1, place_mode == 1, want_grad != 0, R(0));
   if (threadIdx.x == 0) {
     if (obj) obj[p] = C.scal[kObj];
     if (cons) {
@@ -821,8 +838,9 @@ __global__ void __launch_bounds__(kMaxAlThreads) k_validate(const TrajScene<R>* 
   C.bind(smem, L);
   const int64_t p = blockIdx.x;
   al_load(C, g_scene, values, p);
-  al_eval<R, KIND, SPB>(C, tw, prm, false, false, false, R(0));  // FK tables for the current x
-  al_validate<R, KIND, SPB>(C, tw, prm);
+  const auto& tws = twin_smem(smem, L, tw);
+  al_eval<R, KIND, SPB>(C, tws, prm, false, false, false, R(0));  // FK tables for the current x
+  al_validate<R, KIND, SPB>(C, tws, prm);
   if (threadIdx.x == 0) {
     const R wv = C.scal[kWorst];
     violation[p] = wv;
@@ -861,6 +879,7 @@ __global__ void __launch_bounds__(kMaxAlThreads) k_solve_al(const TrajScene<R>* 
   const int p = blockIdx.x;
   if (rec.n_active && p >= *rec.n_active) return;
   al_load(C, g_scene, values, p);
+  const auto& tws = twin_smem(smem, L, tw);
   const TrajScene<R>& sc = *C.sc;
   const ChainDesc<R>& ch = sc.ch;
   const int tid = threadIdx.x;
@@ -887,7 +906,7 @@ __global__ void __launch_bounds__(kMaxAlThreads) k_solve_al(const TrajScene<R>* 
     if (C.flags[0]) break;
     for (int k = 0; k < prm.inner_steps; ++k) {
       const R lr = R(prm.lr_init) + (R(prm.lr_final) - R(prm.lr_init)) * (R(k) / denom);
-      al_eval<R, KIND, SPB>(C, tw, prm, false, prm.place_mode == 1, true, lr);
+      al_eval<R, KIND, SPB>(C, tws, prm, false, prm.place_mode == 1, true, lr);
     }
     // retract pick waypoints to the exact grasp (trajopt.py:1004-1007): one 8-lane tile
     // per segment, lane j = joint j
@@ -901,8 +920,8 @@ __global__ void __launch_bounds__(kMaxAlThreads) k_solve_al(const TrajScene<R>* 
     }
     __syncthreads();
     C.prof.mark(8);  // pick-waypoint polish (+ the last inner step's tail)
-    al_eval<R, KIND, SPB>(C, tw, prm, false, prm.place_mode == 1, false, R(0));
-    al_validate<R, KIND, SPB>(C, tw, prm);
+    al_eval<R, KIND, SPB>(C, tws, prm, false, prm.place_mode == 1, false, R(0));
+    al_validate<R, KIND, SPB>(C, tws, prm);
     C.prof.mark(9);  // re-evaluation + validate (eval marks fold into 0-4)
     if (tid == 0) {
       const int64_t o = (int64_t)outer * P + p;

@@ -31,9 +31,17 @@ __device__ __forceinline__ void twin_reduce_slots(const R* slots, int nv, R* gra
   if constexpr (WG) {
     __syncwarp();
     for (int k = lane; k < nv; k += 32) {
-      R s = R(0);
-      for (int l = 0; l < 32; ++l) s += slots[l * nv + k];
-      grad[k] = s;
+      // 4 interleaved partial sums (fixed order): the 32 loads issue back to back instead
+      // of one dependent load-add chain
+      R s0 = R(0), s1 = R(0), s2 = R(0), s3 = R(0);
+#pragma unroll
+      for (int l = 0; l < 32; l += 4) {
+        s0 += slots[l * nv + k];
+        s1 += slots[(l + 1) * nv + k];
+        s2 += slots[(l + 2) * nv + k];
+        s3 += slots[(l + 3) * nv + k];
+      }
+      grad[k] = (s0 + s1) + (s2 + s3);
     }
   }
 }
