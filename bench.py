@@ -264,8 +264,9 @@ def run_b200(args):
             mdl = as_cost_model(sc.problem, precision=args.precision)
             sol = solve_scene(sc, seed=seed, solver_overrides=over, no_trajopt=True, precision=args.precision,
                               model=mdl, warm_seeds=replan["warm"], comm=comm)
-            if sol.success:
-                replan["warm"] = sol.placement[None, :].copy()
+            if sol.success:  # all returned placements seed the next tick (SPASM_C4_WARM=best: only the best)
+                keep_all = os.environ.get("SPASM_C4_WARM", "all") == "all" and sol.particles is not None
+                replan["warm"] = (sol.particles if keep_all else sol.placement[None, :]).copy()
             replan["tick_ms"].append((time.perf_counter() - t0) * 1e3)
             return sol
 

@@ -49,8 +49,10 @@ class SceneSolution:
     trajectory: object = None
     path_length: Optional[float] = None
     max_violation: Optional[float] = None
-    # B200 extras (not in the reference): work and launch counts for the bench line
+    # B200 extras (not in the reference): work and launch counts for the bench line, and
+    # every satisfying stage-1 particle returned (the replanning loop warm-starts from them)
     stats: dict = field(default_factory=dict)
+    particles: Optional[np.ndarray] = None
 
 
 def solve_scene(scene: Scene, *, seed: int = 0, threads: int = 1, solver_overrides: Optional[dict] = None,
@@ -90,7 +92,7 @@ def solve_scene(scene: Scene, *, seed: int = 0, threads: int = 1, solver_overrid
         best = result.particles[0]
         ok = bool(np.asarray(model.satisfaction(best[None, :], config.epsilon))[0])
         return SceneSolution(ok, time_ms, result.report.restarts, result.report.steps, float(result.costs[0]),
-                             placement=best.copy(), stats=stats)
+                             placement=best.copy(), stats=stats, particles=result.particles.copy())
     from .trajopt import solve_stage2
 
     sol = solve_stage2(scene, result, config, seed, trajopt_overrides, t0, precision=precision)

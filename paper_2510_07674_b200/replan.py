@@ -59,8 +59,8 @@ def replan_loop(ticks: int, *, seed: int = 0, first_tick: int = 0, solver_overri
         tick_ms = (time.perf_counter() - t0) * 1e3
         out.append(Tick(k, bool(sol.success), tick_ms, sol.time_ms, sol.restarts, warm is not None,
                         None if sol.placement is None else sol.placement.copy(), sol.stats))
-        if sol.success:
-            warm = sol.placement.copy()
+        if sol.success:  # warm-start the next tick from every returned placement
+            warm = (sol.particles if sol.particles is not None else sol.placement[None, :]).copy()
     return out, warm
 
 
