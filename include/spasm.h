@@ -52,7 +52,8 @@ int spasm_version(void);
 /* Process-wide tuning switches (not in the reference; results stay within the parity
  * tolerances under every setting). "stage1_tile": -1 auto (default: on), 0 = generic
  * stage-1 kernels only, 1..4 = on (the fp32 tetris tile kernels, 4 lanes per particle;
- * stage1_tile.cuh). */
+ * stage1_tile.cuh). "graphs": 1 (default) runs each spasm_solve restart as a cached CUDA
+ * graph, 0 launches its kernels one by one (same results). */
 int spasm_set_option(const char* key, int value);
 
 /* ---- model construction ------------------------------------------------------

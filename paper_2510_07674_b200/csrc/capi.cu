@@ -24,6 +24,9 @@ const char* last_error() { return g_last_error.c_str(); }
 
 static int g_stage1_tile = -1;  // spasm_set_option("stage1_tile", ...)
 int stage1_tile_mode() { return g_stage1_tile; }
+static int g_graphs = 1;       // spasm_set_option("graphs", ...): CUDA-graph the stage-1 restart
+static thread_local const RestartParams* g_restart_override = nullptr;
+const RestartParams* restart_override() { return g_restart_override; }
 
 
 // ---- small helper kernels for the solve loop --------------------------------------
@@ -194,36 +197,98 @@ static int solve_impl(Model& m, const spasm_solve_config& cfg, const double* war
   const int per_restart = cfg.k_lin + cfg.k_quad;
   int rc = SPASM_NO_SOLUTION;
   std::memset(rep, 0, sizeof(*rep));
-  for (int restart = 0; restart < cfg.max_restarts; ++restart) {
-    const Pcg64State st = restart_state(cfg.seed, (uint64_t)restart);
+  const bool tr = trace_cost != nullptr && cfg.n_traced > 0;
+
+  // One restart's device work on stream ss, ending with the D2H copy of the result block.
+  auto body = [&](int restart, const Pcg64State& st, cudaStream_t ss) -> int {
     int r = launch_sample_eval<R>(m, st, 0, cfg.n, n_warm ? warm_dev : nullptr, n_warm, cfg.sampler, cfg.seed,
-                                  (uint32_t)restart, values, keys0, idx0, s);
+                                  (uint32_t)restart, values, keys0, idx0, ss);
     if (r) return r;
     bool in1 = false;
-    if ((r = launch_sort<R>(keys0, idx0, keys1, idx1, cfg.n, hist, &in1, s))) return r;
+    if ((r = launch_sort<R>(keys0, idx0, keys1, idx1, cfg.n, hist, &in1, ss))) return r;
     const uint32_t* top = in1 ? idx1 : idx0;
-    SPASM_CUDA_TRY(cudaMemsetAsync(res, 0, 64, s));
-    const bool tr = trace_cost != nullptr && cfg.n_traced > 0;
+    SPASM_CUDA_TRY(cudaMemsetAsync(res, 0, 64, ss));
     if ((r = launch_schedule<R>(m, values, top, cfg.m, cfg.k_lin, cfg.k_quad, cfg.eta_init, cfg.alpha, cfg.epsilon,
                                 opt_values, opt_cost, flagged, counters + 1, tr ? trace_cost : nullptr,
-                                tr ? trace_sat : nullptr, tr ? cfg.n_traced : 0, step_rule(cfg, restart), s)))
+                                tr ? trace_sat : nullptr, tr ? cfg.n_traced : 0, step_rule(cfg, restart), ss)))
       return r;
     if (tr && trace_ids) {
-      k_trace_ids<<<ceil_div(cfg.n_traced, 256), 256, 0, s>>>(top, cfg.n_traced, trace_ids);
+      k_trace_ids<<<ceil_div(cfg.n_traced, 256), 256, 0, ss>>>(top, cfg.n_traced, trace_ids);
       SPASM_CHECK_LAUNCH();
     }
-    if ((r = launch_sat_keys<R>(opt_cost, cfg.m, cfg.epsilon, sk0, sv0, counters, s))) return r;
+    if ((r = launch_sat_keys<R>(opt_cost, cfg.m, cfg.epsilon, sk0, sv0, counters, ss))) return r;
     bool sin1 = false;
-    if ((r = launch_sort<R>(sk0, sv0, sk1, sv1, cfg.m, hist, &sin1, s))) return r;
+    if ((r = launch_sort<R>(sk0, sv0, sk1, sv1, cfg.m, hist, &sin1, ss))) return r;
     const uint32_t* order = sin1 ? sv1 : sv0;
-    k_gather_chosen<R><<<cfg.p_return, 32, 0, s>>>(order, counters, cfg.p_return, opt_values, opt_cost, top, D,
-                                                   chosen_vals, out_vals, out_cost, out_idx);
+    k_gather_chosen<R><<<cfg.p_return, 32, 0, ss>>>(order, counters, cfg.p_return, opt_values, opt_cost, top, D,
+                                                    chosen_vals, out_vals, out_cost, out_idx);
     SPASM_CHECK_LAUNCH();
     // independent soundness re-check: fresh QUADRATIC evaluation of the chosen rows
-    if ((r = launch_evaluate<R>(m, chosen_vals, cfg.p_return, 1, recheck, s))) return r;
-    k_copy_recheck<R><<<ceil_div(cfg.p_return, 128), 128, 0, s>>>(recheck, cfg.p_return, out_recheck);
+    if ((r = launch_evaluate<R>(m, chosen_vals, cfg.p_return, 1, recheck, ss))) return r;
+    k_copy_recheck<R><<<ceil_div(cfg.p_return, 128), 128, 0, ss>>>(recheck, cfg.p_return, out_recheck);
     SPASM_CHECK_LAUNCH();
-    SPASM_CUDA_TRY(cudaMemcpyAsync(host, res, L.res_bytes, cudaMemcpyDeviceToHost, s));
+    SPASM_CUDA_TRY(cudaMemcpyAsync(host, res, L.res_bytes, cudaMemcpyDeviceToHost, ss));
+    return SPASM_OK;
+  };
+
+  // CUDA graph of the restart (reference GD step, no trace): captured once per (model,
+  // workspace, config) and relaunched for every restart and every later solve with the
+  // same shapes; the restart's PCG64 state / seed / index travel through device memory
+  // (RestartParams), refreshed by the graph's first node from pinned host memory.
+  const bool use_graph = g_graphs && !tr && step_rule(cfg, 0).is_reference();
+  if (use_graph) {
+    Model::GraphKeyPod key;
+    std::memset(&key, 0, sizeof(key));
+    key.ws = ws;
+    key.host = host;
+    key.dtype = (int)sizeof(R);
+    key.n = cfg.n;
+    key.m = cfg.m;
+    key.k_lin = cfg.k_lin;
+    key.k_quad = cfg.k_quad;
+    key.eta = cfg.eta_init;
+    key.alpha = cfg.alpha;
+    key.eps = cfg.epsilon;
+    key.p_return = cfg.p_return;
+    key.sampler = cfg.sampler;
+    key.n_warm = n_warm;
+    key.tile = stage1_tile_mode();
+    if (!m.gexec || std::memcmp(&key, &m.gkey, sizeof(key)) != 0) {
+      if (m.gexec) cudaGraphExecDestroy(m.gexec);
+      m.gexec = nullptr;
+      if (!m.cap) SPASM_CUDA_TRY(cudaStreamCreateWithFlags(&m.cap, cudaStreamNonBlocking));
+      if (!m.rp_dev) SPASM_CUDA_TRY(cudaMalloc(&m.rp_dev, sizeof(RestartParams)));
+      if (!m.rp_host) SPASM_CUDA_TRY(cudaMallocHost(&m.rp_host, sizeof(RestartParams)));
+      SPASM_CUDA_TRY(cudaStreamBeginCapture(m.cap, cudaStreamCaptureModeThreadLocal));
+      cudaMemcpyAsync(m.rp_dev, m.rp_host, sizeof(RestartParams), cudaMemcpyHostToDevice, m.cap);
+      g_restart_override = m.rp_dev;
+      const int r = body(0, restart_state(cfg.seed, 0), m.cap);
+      g_restart_override = nullptr;
+      cudaGraph_t graph = nullptr;
+      const cudaError_t ec = cudaStreamEndCapture(m.cap, &graph);
+      if (r || ec != cudaSuccess) {
+        if (graph) cudaGraphDestroy(graph);
+        if (r) return r;
+        SPASM_CUDA_TRY(ec);
+      }
+      const cudaError_t ei = cudaGraphInstantiate(&m.gexec, graph, 0);
+      cudaGraphDestroy(graph);
+      SPASM_CUDA_TRY(ei);
+      m.gkey = key;
+    }
+  }
+
+  for (int restart = 0; restart < cfg.max_restarts; ++restart) {
+    const Pcg64State st = restart_state(cfg.seed, (uint64_t)restart);
+    if (use_graph) {
+      m.rp_host->st = st;
+      m.rp_host->seed = cfg.seed;
+      m.rp_host->restart = (uint32_t)restart;
+      SPASM_CUDA_TRY(cudaGraphLaunch(m.gexec, s));
+    } else {
+      const int r = body(restart, st, s);
+      if (r) return r;
+    }
     SPASM_CUDA_TRY(cudaStreamSynchronize(s));
 
     const unsigned int* hc = reinterpret_cast<const unsigned int*>(host);
@@ -424,6 +489,11 @@ extern "C" {
 
 int spasm_set_option(const char* key, int value) {
   SPASM_REQUIRE(key != nullptr, "null option key");
+  if (std::strcmp(key, "graphs") == 0) {
+    SPASM_REQUIRE(value == 0 || value == 1, "graphs must be 0 or 1");
+    g_graphs = value;
+    return SPASM_OK;
+  }
   if (std::strcmp(key, "stage1_tile") == 0) {
     SPASM_REQUIRE(value >= -1 && value <= 4, "stage1_tile must be -1 (auto), 0 (off) or 1..4");
     g_stage1_tile = value;
@@ -554,6 +624,10 @@ int spasm_tower_model_create(spasm_model** out, int n_blocks, double side, doubl
 void spasm_model_destroy(spasm_model* model) {
   if (!model) return;
   if (model->pinned) cudaFreeHost(model->pinned);
+  if (model->gexec) cudaGraphExecDestroy(model->gexec);
+  if (model->cap) cudaStreamDestroy(model->cap);
+  if (model->rp_dev) cudaFree(model->rp_dev);
+  if (model->rp_host) cudaFreeHost(model->rp_host);
   delete model;
 }
 

@@ -1,6 +1,7 @@
 // Host-side model object behind the opaque spasm_model handle.
 #pragma once
 #include "scene.cuh"
+#include "rng.cuh"
 
 namespace spasm {
 
@@ -23,6 +24,22 @@ struct Model {
   // pinned staging for solve results (grown on demand, never inside a kernel sequence)
   void* pinned = nullptr;
   size_t pinned_bytes = 0;
+  // cached CUDA graph of one stage-1 restart (capi.cu solve_impl) and what it was built for
+  cudaGraphExec_t gexec = nullptr;
+  cudaStream_t cap = nullptr;
+  RestartParams* rp_dev = nullptr;
+  RestartParams* rp_host = nullptr;
+  struct GraphKeyPod {
+    void* ws;
+    void* host;
+    int dtype;
+    int64_t n, m;
+    int k_lin, k_quad;
+    double eta, alpha, eps;
+    int p_return, sampler;
+    int64_t n_warm;
+    int tile;
+  } gkey{};
 
   template <typename R> const TetrisScene<R>& tetris() const;
   template <typename R> const TowerScene<R>& tower() const;

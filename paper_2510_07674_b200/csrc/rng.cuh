@@ -19,6 +19,15 @@ struct Pcg64State {
   uint64_t inc_hi, inc_lo;      // 128-bit odd increment
 };
 
+// The restart-dependent sampler inputs read from device memory instead of kernel arguments,
+// so one captured CUDA graph of the stage-1 restart serves every restart (capi.cu).
+struct RestartParams {
+  Pcg64State st;
+  uint64_t seed;
+  uint32_t restart;
+  uint32_t pad;
+};
+
 __host__ __device__ __forceinline__ u128 make_u128(uint64_t hi, uint64_t lo) {
   return ((u128)hi << 64) | (u128)lo;
 }

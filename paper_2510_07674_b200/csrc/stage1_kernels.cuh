@@ -126,7 +126,13 @@ template <class E, typename R>
 __global__ void k_sample_eval(const typename E::Scene sc, const Bounds64 bd, Pcg64State st, int64_t row_offset,
                               int64_t N, const double* __restrict__ warm, int64_t n_warm, int use_philox,
                               uint64_t philox_seed, uint32_t restart, R* __restrict__ values,
-                              typename KeyOf<R>::type* __restrict__ keys, uint32_t* __restrict__ idx) {
+                              typename KeyOf<R>::type* __restrict__ keys, uint32_t* __restrict__ idx,
+                              const RestartParams* __restrict__ rp) {
+  if (rp) {  // graph launch: restart inputs from device memory
+    st = rp->st;
+    philox_seed = rp->seed;
+    restart = rp->restart;
+  }
   const int bs = blockDim.x;
   const int D = sc.dim;
   R* base = particle_smem<R>(0);
@@ -148,7 +154,13 @@ __global__ void k_sample_eval(const typename E::Scene sc, const Bounds64 bd, Pcg
 template <typename R>
 __global__ void k_sample(const Bounds64 bd, Pcg64State st, int64_t row_offset, const uint32_t* __restrict__ rows,
                          int64_t N, int D, const double* __restrict__ warm, int64_t n_warm, int use_philox,
-                         uint64_t philox_seed, uint32_t restart, R* __restrict__ values) {
+                         uint64_t philox_seed, uint32_t restart, R* __restrict__ values,
+                         const RestartParams* __restrict__ rp) {
+  if (rp) {  // graph launch: restart inputs from device memory
+    st = rp->st;
+    philox_seed = rp->seed;
+    restart = rp->restart;
+  }
   const int bs = blockDim.x;
   R* base = particle_smem<R>(0);
   const int64_t p0 = (int64_t)blockIdx.x * bs;

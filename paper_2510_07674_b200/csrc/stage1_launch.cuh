@@ -9,6 +9,10 @@
 
 namespace spasm {
 
+// Device-resident restart inputs for the sampler kernels while a stage-1 restart is being
+// captured as a CUDA graph (capi.cu); nullptr otherwise.
+const RestartParams* restart_override();
+
 // Stage-1 tile-kernel switch (spasm_set_option("stage1_tile", v)): -1 auto, 0 generic
 // kernel only, 1..4 force a tile variant (stage1tile_f32.cu).
 int stage1_tile_mode();
@@ -121,7 +125,8 @@ int launch_sample_eval(const Model& m, const Pcg64State& st, int64_t row_offset,
     const int bs = pick_block(N, per);
     allow_big_smem(k_sample_eval<E, R>);
     k_sample_eval<E, R><<<ceil_div(N, bs), bs, per * bs, s>>>(sc, m.bounds, st, row_offset, N, warm, n_warm,
-                                                            use_philox, seed, restart, values, keys, idx);
+                                                            use_philox, seed, restart, values, keys, idx,
+                                                            restart_override());
     SPASM_CHECK_LAUNCH();
     return SPASM_OK;
   });
@@ -173,7 +178,7 @@ int launch_sample(const Bounds64& bd, int D, const Pcg64State& st, int64_t row_o
   const int bs = pick_block(N, per);
   allow_big_smem(k_sample<R>);
   k_sample<R><<<ceil_div(N, bs), bs, per * bs, s>>>(bd, st, row_offset, rows, N, D, warm, n_warm, use_philox, seed,
-                                                    restart, values);
+                                                    restart, values, restart_override());
   SPASM_CHECK_LAUNCH();
   return SPASM_OK;
 }
