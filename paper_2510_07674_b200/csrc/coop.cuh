@@ -69,14 +69,38 @@ struct TileFrame {
   R Ree[9];
 };
 
+// The chain constants one tile lane needs every FK (its joint's axis / offset / limits and
+// the uniform tool transform), held in registers across the DLS iterations instead of
+// re-read from the shared-memory ChainDesc on every iteration's critical path.
 template <typename R>
-__device__ __forceinline__ void tile_fk(const Tile& tl, const ChainDesc<R>& ch, R qj, TileFrame<R>& f) {
+struct LaneChain {
+  int J, full;
+  R ax[3], off[3], lo, hi, tool_t[3], tool_R[9];
+  __device__ __forceinline__ void load(const ChainDesc<R>& ch, int j) {
+    J = ch.J;
+    const int jj = j < ch.J ? j : 0;
+    full = j < ch.J ? ch.full_circle[jj] : 0;
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      ax[c] = ch.axis[jj][c];
+      off[c] = ch.offset[jj][c];
+      tool_t[c] = ch.tool_t[c];
+    }
+#pragma unroll
+    for (int c = 0; c < 9; ++c) tool_R[c] = ch.tool_R[c];
+    lo = ch.lo[jj];
+    hi = ch.hi[jj];
+  }
+};
+
+template <typename R>
+__device__ __forceinline__ void tile_fk(const Tile& tl, const LaneChain<R>& ch, R qj, TileFrame<R>& f) {
   const int J = ch.J;
   const int j = tl.j;
   const bool live = j < J;
   R Rj[9];
   if (live) {
-    rodrigues(ch.axis[j], qj, Rj);
+    rodrigues(ch.ax, qj, Rj);
   } else {
 #pragma unroll
     for (int k = 0; k < 9; ++k) Rj[k] = (k % 4 == 0) ? R(1) : R(0);
@@ -105,8 +129,8 @@ __device__ __forceinline__ void tile_fk(const Tile& tl, const ChainDesc<R>& ch, 
   }
   R t[3] = {R(0), R(0), R(0)};
   if (live) {
-    mat3_vec(M, ch.offset[j], t);
-    mat3_vec(M, ch.axis[j], f.z);
+    mat3_vec(M, ch.off, t);
+    mat3_vec(M, ch.ax, f.z);
   } else {
     f.z[0] = f.z[1] = f.z[2] = R(0);
   }
@@ -133,6 +157,13 @@ __device__ __forceinline__ void tile_fk(const Tile& tl, const ChainDesc<R>& ch, 
   f.ee[1] = pf[1] + tt[1];
   f.ee[2] = pf[2] + tt[2];
   mat3_mul(Pf, ch.tool_R, f.Ree);
+}
+
+template <typename R>
+__device__ __forceinline__ void tile_fk(const Tile& tl, const ChainDesc<R>& ch, R qj, TileFrame<R>& f) {
+  LaneChain<R> lc;
+  lc.load(ch, tl.j);
+  tile_fk(tl, lc, qj, f);
 }
 
 // world centre of arm sphere s (owned by link j = this lane): p_j + P_j * local_s
@@ -201,10 +232,12 @@ __device__ bool tile_ik(const Tile& tl, const ChainDesc<R>& ch, R& qj, const R t
                         R* score) {
   const int j = tl.j;
   const bool live = j < ch.J;
+  LaneChain<R> lc;
+  lc.load(ch, j);
   TileFrame<R> f;
   R prev1 = qj, prev2 = qj;
   for (int it = 0; it < max_iters; ++it) {
-    tile_fk(tl, ch, qj, f);
+    tile_fk(tl, lc, qj, f);
     const R pe[3] = {tp[0] - f.ee[0], tp[1] - f.ee[1], tp[2] - f.ee[2]};
     const R ye = wrap_yaw(ty - yaw_of(f.Ree));
     const R pn = Math<R>::sqrt_((pe[0] * pe[0] + pe[1] * pe[1]) + pe[2] * pe[2]);
@@ -217,11 +250,11 @@ __device__ bool tile_ik(const Tile& tl, const ChainDesc<R>& ch, R& qj, const R t
     const R dq = tile_dls<R, 4>(tl, col, e4, damping);
     if (live) {
       const R v = qj + dq;
-      qj = v < ch.lo[j] ? ch.lo[j] : (v > ch.hi[j] ? ch.hi[j] : v);
+      qj = v < lc.lo ? lc.lo : (v > lc.hi ? lc.hi : v);
     }
     if (tile_settled(tl, qj, prev1, prev2, it, max_iters)) break;
   }
-  tile_fk(tl, ch, qj, f);
+  tile_fk(tl, lc, qj, f);
   const R pe[3] = {tp[0] - f.ee[0], tp[1] - f.ee[1], tp[2] - f.ee[2]};
   const R pn = Math<R>::sqrt_((pe[0] * pe[0] + pe[1] * pe[1]) + pe[2] * pe[2]);
   const R ye = fabs(wrap_yaw(ty - yaw_of(f.Ree)));
@@ -243,6 +276,8 @@ __device__ bool tile_polish(const Tile& tl, const ChainDesc<R>& ch, R& qj, const
   const bool live = j < ch.J;
   const R cos_tol = R(0.99998750002604164);  // cos(0.005)
   const R two_pi = R(6.283185307179586476925286766559);
+  LaneChain<R> lc;
+  lc.load(ch, j);
   TileFrame<R> f;
   R prev1 = qj, prev2 = qj;
   for (int it = 0; it < kPolishMaxIters; ++it) {
@@ -254,7 +289,7 @@ __device__ bool tile_polish(const Tile& tl, const ChainDesc<R>& ch, R& qj, const
       }
       if (__shfl_sync(tl.mask, stop, 0, kTile)) return false;
     }
-    tile_fk(tl, ch, qj, f);
+    tile_fk(tl, lc, qj, f);
     const R pe[3] = {tp[0] - f.ee[0], tp[1] - f.ee[1], tp[2] - f.ee[2]};
     const R ye = wrap_yaw(ty - yaw_of(f.Ree));
     const R ax[3] = {f.Ree[2], f.Ree[5], f.Ree[8]};
@@ -269,12 +304,12 @@ __device__ bool tile_polish(const Tile& tl, const ChainDesc<R>& ch, R& qj, const
     const R dq = tile_dls<R, 5>(tl, col, e5, R(kIkDamping));
     if (live) {
       R v = qj + dq;
-      if (ch.full_circle[j]) v = ch.lo[j] + np_mod_pos(v - ch.lo[j], two_pi);
-      qj = v < ch.lo[j] ? ch.lo[j] : (v > ch.hi[j] ? ch.hi[j] : v);
+      if (lc.full) v = lc.lo + np_mod_pos(v - lc.lo, two_pi);
+      qj = v < lc.lo ? lc.lo : (v > lc.hi ? lc.hi : v);
     }
     if (tile_settled(tl, qj, prev1, prev2, it, kPolishMaxIters)) break;
   }
-  tile_fk(tl, ch, qj, f);
+  tile_fk(tl, lc, qj, f);
   const R pe[3] = {tp[0] - f.ee[0], tp[1] - f.ee[1], tp[2] - f.ee[2]};
   const R pn = Math<R>::sqrt_((pe[0] * pe[0] + pe[1] * pe[1]) + pe[2] * pe[2]);
   if (completed) *completed = true;
