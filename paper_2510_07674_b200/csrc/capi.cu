@@ -235,7 +235,7 @@ static int solve_impl(Model& m, const spasm_solve_config& cfg, const double* war
   // workspace, config) and relaunched for every restart and every later solve with the
   // same shapes; the restart's PCG64 state / seed / index travel through device memory
   // (RestartParams), refreshed by the graph's first node from pinned host memory.
-  const bool use_graph = g_graphs && !tr && step_rule(cfg, 0).is_reference();
+  bool use_graph = g_graphs && !tr && step_rule(cfg, 0).is_reference();
   if (use_graph) {
     Model::GraphKeyPod key;
     std::memset(&key, 0, sizeof(key));
@@ -253,6 +253,15 @@ static int solve_impl(Model& m, const spasm_solve_config& cfg, const double* war
     key.sampler = cfg.sampler;
     key.n_warm = n_warm;
     key.tile = stage1_tile_mode();
+    const bool cached = m.gexec && std::memcmp(&key, &m.gkey, sizeof(key)) == 0;
+    // capture only from the second solve with the same shapes: a model solved once (e.g. a
+    // replanning tick's fresh model) never pays for a capture it would not reuse
+    const bool repeat = std::memcmp(&key, &m.gkey_seen, sizeof(key)) == 0;
+    m.gkey_seen = key;
+    if (!cached && !repeat) use_graph = false;
+  }
+  if (use_graph) {
+    const Model::GraphKeyPod& key = m.gkey_seen;
     if (!m.gexec || std::memcmp(&key, &m.gkey, sizeof(key)) != 0) {
       if (m.gexec) cudaGraphExecDestroy(m.gexec);
       m.gexec = nullptr;

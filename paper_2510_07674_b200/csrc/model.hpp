@@ -39,7 +39,7 @@ struct Model {
     int p_return, sampler;
     int64_t n_warm;
     int tile;
-  } gkey{};
+  } gkey{}, gkey_seen{};
 
   template <typename R> const TetrisScene<R>& tetris() const;
   template <typename R> const TowerScene<R>& tower() const;
