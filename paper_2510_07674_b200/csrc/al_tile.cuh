@@ -256,6 +256,7 @@ __device__ void al_eval(AlCtx<R>& C, const typename TwinSceneOf<R, KIND>::type& 
   const int w = tid >> 3;
   const bool is_wp = !is_aux && w < W;
   const Tile tl = Tile::make();
+  const Tile tlw = Tile::make_warp();  // for the calls every lane of the tile warps reaches
   const int j = tl.j;
   const int b = is_wp ? w / T : 0;
   const int t = is_wp ? w - b * T : 0;
@@ -272,7 +273,7 @@ __device__ void al_eval(AlCtx<R>& C, const typename TwinSceneOf<R, KIND>::type& 
     const int wq = is_wp ? w : 0;  // padding tiles mirror waypoint 0 (no writes)
     const R qj = j < J ? C.x[wq * kXS + j] : R(0);
     TileFrame<R> f;
-    tile_fk(tl, ch, qj, f);
+    tile_fk(tlw, ch, qj, f);
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
       st.z[c] = f.z[c];
@@ -303,7 +304,7 @@ __device__ void al_eval(AlCtx<R>& C, const typename TwinSceneOf<R, KIND>::type& 
     // path length (trajopt.py:474-476): tile sum of the leg's squared components
     R dv = R(0);
     if (is_wp && t < T - 1 && j < J) dv = C.x[(wq + 1) * kXS + j] - qj;
-    const R s2 = tl.sum(dv * dv);
+    const R s2 = tlw.sum(dv * dv);
     if (is_wp && t < T - 1) {
       const R ln = Math<R>::sqrt_(s2);
       if (j == 0) obj_w += ln;
@@ -492,7 +493,7 @@ __device__ void al_eval(AlCtx<R>& C, const typename TwinSceneOf<R, KIND>::type& 
       for (int d = 1; d < kTile; d <<= 1) {
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
-          const R gv = tl.down(G[c], d), mv = tl.down(Mv[c], d);
+          const R gv = tlw.down(G[c], d), mv = tlw.down(Mv[c], d);
           if (j + d < kTile) {
             G[c] += gv;
             Mv[c] += mv;
@@ -520,8 +521,8 @@ __device__ void al_eval(AlCtx<R>& C, const typename TwinSceneOf<R, KIND>::type& 
       }
 #pragma unroll
       for (int c = 0; c < 3; ++c) {
-        Gh[c] = tl.sum(Gh[c]);
-        Mh[c] = tl.sum(Mh[c]);
+        Gh[c] = tlw.sum(Gh[c]);
+        Mh[c] = tlw.sum(Mh[c]);
       }
       cross3(st.o, Gh, og);
       st.gblk = (st.z[0] * (Mh[0] - og[0]) + st.z[1] * (Mh[1] - og[1])) + st.z[2] * (Mh[2] - og[2]);

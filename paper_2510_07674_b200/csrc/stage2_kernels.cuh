@@ -95,9 +95,12 @@ __global__ void __launch_bounds__(1024) k_ik_group(const TrajScene<R>* __restric
   const int grp = blockIdx.x;
   const int a = grp / n_targets, t = grp - a * n_targets;
   const int J = ch.J;
-  const Tile tl = Tile::make();
+  // every lane of a restart's warp runs the tile (4 identical replicas of the 8-lane tile),
+  // so its shuffles can name the whole warp (Tile::make_warp); lanes 0-7 write results
+  const Tile tl = Tile::make_warp();
   const int tile = threadIdx.x >> 5;
   const bool tile_lane = (threadIdx.x & 31) < kTile;
+  const bool lane0 = (threadIdx.x & 31) == 0;
   R tp[3], ty;
   if (tpos_in) {
     tp[0] = (R)tpos_in[3 * t];
@@ -110,7 +113,7 @@ __global__ void __launch_bounds__(1024) k_ik_group(const TrajScene<R>* __restric
   R qj = R(0);
   bool pol_spec = true, spec_done = false;
   R ik_q = R(0);
-  if (tile < restarts && tile_lane) {
+  if (tile < restarts) {
     if (tl.j < J) {
       // seeds[t] = uniform(lower, upper, (restarts, dof)) of SeedSequence(seed, (t,)) (robot.py:255-257)
       Pcg64 g;
@@ -125,7 +128,7 @@ __global__ void __launch_bounds__(1024) k_ik_group(const TrajScene<R>* __restric
     // speculation order: (fp32 image of the key, restart); the exact winner is s_best below
     const unsigned long long mine = ((unsigned long long)order_key((float)key) << 32) | (unsigned)tile;
     int last = 0, lead = 0;
-    if (tl.j == 0) {
+    if (lane0) {
       s_key[tile] = key;
       s_score[tile] = score;
       s_ok[tile] = ok;
@@ -133,9 +136,9 @@ __global__ void __launch_bounds__(1024) k_ik_group(const TrajScene<R>* __restric
       lead = atomicMin(&s_cur, mine) > mine;
       last = atomicAdd(&s_done, 1) == restarts - 1;
     }
-    last = __shfl_sync(tl.mask, last, 0, kTile);
-    lead = __shfl_sync(tl.mask, lead, 0, kTile);
-    if (last && tl.j == 0) {  // the last restart to finish picks the first minimum (np.argmin)
+    last = __shfl_sync(0xffffffffu, last, 0);
+    lead = __shfl_sync(0xffffffffu, lead, 0);
+    if (last && lane0) {  // the last restart to finish picks the first minimum (np.argmin)
       __threadfence_block();
       int b = 0;
       for (int r = 1; r < restarts; ++r)
@@ -149,7 +152,7 @@ __global__ void __launch_bounds__(1024) k_ik_group(const TrajScene<R>* __restric
     if (polish && lead) pol_spec = tile_polish<R>(tl, ch, qj, tp, ty, &s_best, tile, &s_cur, mine, &spec_done);
   }
   __syncthreads();
-  if (tile != s_best || !tile_lane) return;
+  if (tile != s_best) return;  // the whole winner warp stays: the polish below shuffles warp-wide
   bool pol = true;
   R pen = R(0);
   if (polish) {
@@ -160,6 +163,7 @@ __global__ void __launch_bounds__(1024) k_ik_group(const TrajScene<R>* __restric
     pol = pol_spec;
     if (score_statics && sc.n_static > 0) pen = tile_arm_worst_pen<R>(tl, ch, qj, sc.st_c, sc.st_r, sc.n_static);
   }
+  if (!tile_lane) return;
   if (tl.j < J) reinterpret_cast<R*>(out.sol)[(int64_t)grp * J + tl.j] = qj;
   if (tl.j == 0) {
     out.ik_ok[grp] = (uint8_t)s_ok[s_best];
