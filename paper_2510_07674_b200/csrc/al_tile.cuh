@@ -370,18 +370,20 @@ __device__ void al_eval(AlCtx<R>& C, const typename TwinSceneOf<R, KIND>::type& 
         C.scal[kCplace] = cpl;
       }
     }
-  } else if (is_wp) {
+  } else if (w < C.L.NW / kTile) {
     // every sphere of the waypoint against the fixed obstacles, the obstacle list split over
     // the tile's 8 lanes and tile-summed (the per-lane sphere loop left one lane with all
-    // the held-block pairs on top of its link's spheres)
+    // the held-block pairs on top of its link's spheres). Padding tiles mirror waypoint 0
+    // without writing, so every lane of the tile warps reaches the warp-mask sums.
+    const int wq = is_wp ? w : 0;
     for (int s = 0; s < S; ++s) {
       R gg[3] = {R(0), R(0), R(0)};
-      R v = pens_fixed_lane(sc, C.armw + (w * S + s) * 3, ch.arm_r[s], f0, f1, quad, j, gg);
-      v = tl.sum(v);
-      gg[0] = tl.sum(gg[0]);
-      gg[1] = tl.sum(gg[1]);
-      gg[2] = tl.sum(gg[2]);
-      if (j == 0) {
+      R v = pens_fixed_lane(sc, C.armw + (wq * S + s) * 3, ch.arm_r[s], f0, f1, quad, j, gg);
+      v = tlw.sum(v);
+      gg[0] = tlw.sum(gg[0]);
+      gg[1] = tlw.sum(gg[1]);
+      gg[2] = tlw.sum(gg[2]);
+      if (is_wp && j == 0) {
         carm += v;
         R* ga = C.ga + (w * S + s) * 3;
         ga[0] = gg[0];
@@ -415,11 +417,14 @@ __device__ void al_eval(AlCtx<R>& C, const typename TwinSceneOf<R, KIND>::type& 
   st.garm = R(0);
   st.gblk = R(0);
   if (!is_aux && w < C.L.NW / kTile) {
-    if (manip && is_wp) {
-      for (int jb = 0; jb < b; ++jb) {
+    if (manip) {
+      // uniform trip count over the warp (blocks jb < B - 1; a waypoint of segment b uses
+      // jb < b) so the partial sums below can use the warp-mask shuffles
+      for (int jb = 0; jb + 1 < B; ++jb) {
+        const bool act = is_wp && jb < b;
         const R cj = C.cp[jb], sj = C.sp[jb];
         R A[4] = {R(0), R(0), R(0), R(0)}, H[4] = {R(0), R(0), R(0), R(0)};
-        for (int q = sc.blk_start[jb]; q < sc.blk_start[jb + 1]; ++q) {
+        for (int q = act ? sc.blk_start[jb] : 0; q < (act ? sc.blk_start[jb + 1] : 0); ++q) {
           const R px = C.pl[3 * q], py = C.pl[3 * q + 1], pz = C.pl[3 * q + 2], rq = sc.br[q];
           const R drx = -sj * sc.bu[q][0] - cj * sc.bu[q][1];
           const R dry = cj * sc.bu[q][0] - sj * sc.bu[q][1];
@@ -463,8 +468,8 @@ __device__ void al_eval(AlCtx<R>& C, const typename TwinSceneOf<R, KIND>::type& 
         if (want_grad) {  // tile-reduce, lane 0 stores [class][block jb][G xyz | G yaw]
 #pragma unroll
           for (int i = 0; i < 4; ++i) {
-            const R av = tl.sum(A[i]), hv = tl.sum(H[i]);
-            if (j == 0) {
+            const R av = tlw.sum(A[i]), hv = tlw.sum(H[i]);
+            if (act && j == 0) {
               C.pg[((w * 2 + 0) * B + jb) * 4 + i] = av;
               C.pg[((w * 2 + 1) * B + jb) * 4 + i] = hv;
             }
