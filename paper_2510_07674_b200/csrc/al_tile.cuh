@@ -914,9 +914,19 @@ __global__ void __launch_bounds__(kMaxAlThreads) k_solve_al(const TrajScene<R>* 
       const R lr = R(prm.lr_init) + (R(prm.lr_final) - R(prm.lr_init)) * (R(k) / denom);
       al_eval<R, KIND, SPB>(C, tws, prm, false, prm.place_mode == 1, true, lr);
     }
-    // retract pick waypoints to the exact grasp (trajopt.py:1004-1007): one 8-lane tile
-    // per segment, lane j = joint j
-    if (manip && (tid >> 3) < sc.B) {
+    // retract pick waypoints to the exact grasp (trajopt.py:1004-1007), lane j = joint j.
+    // With at least B tile warps, warp bb polishes segment bb as 4 identical 8-lane replicas
+    // (warp-mask shuffles, replicas exit together); else one tile per segment.
+    if (manip && L.NW / 32 >= sc.B) {
+      if ((tid >> 5) < sc.B) {
+        const Tile tlw = Tile::make_warp();
+        const int bb = tid >> 5;
+        const int w0 = bb * T;
+        R qj = tlw.j < J ? C.x[w0 * kXS + tlw.j] : R(0);
+        tile_polish<R>(tlw, ch, qj, sc.pick_pos[bb], sc.pick_yaw[bb]);
+        if ((tid & 31) < kTile && tlw.j < J) C.x[w0 * kXS + tlw.j] = qj;
+      }
+    } else if (manip && (tid >> 3) < sc.B) {
       const Tile tl = Tile::make();
       const int bb = tid >> 3;
       const int w0 = bb * T;
