@@ -391,15 +391,16 @@ __device__ void al_eval(AlCtx<R>& C, const typename TwinSceneOf<R, KIND>::type& 
         ga[2] = gg[2];
       }
     }
-    if (interior) {
-      for (int s = 0; s < nh; ++s) {
+    if (manip) {  // held-block spheres: uniform bound SB over the warp, inactive slots add zero
+      for (int s = 0; s < SBn; ++s) {
+        const bool act = interior && s < nh;
         R gg[3] = {R(0), R(0), R(0)};
-        R v = pens_fixed_lane(sc, C.hp + (w * SBn + s) * 3, sc.br[h0 + s], f0, f1, quad, j, gg);
-        v = tl.sum(v);
-        gg[0] = tl.sum(gg[0]);
-        gg[1] = tl.sum(gg[1]);
-        gg[2] = tl.sum(gg[2]);
-        if (j == 0) {
+        R v = act ? pens_fixed_lane(sc, C.hp + (w * SBn + s) * 3, sc.br[h0 + s], f0, f1, quad, j, gg) : R(0);
+        v = tlw.sum(v);
+        gg[0] = tlw.sum(gg[0]);
+        gg[1] = tlw.sum(gg[1]);
+        gg[2] = tlw.sum(gg[2]);
+        if (act && j == 0) {
           cblk += v;
           R* gh = C.gh + (w * SBn + s) * 3;
           gh[0] = gg[0];
