@@ -151,7 +151,7 @@ __device__ R twin_tower_warp(const TowerScene<R>& sc, const R* rows, R* grad, R*
     for (int k = 0; k < nv; ++k) my[k] = R(0);
   R cost = R(0);
   const int n_stab = n - 1, n_pair = n * (n - 1) / 2;
-  const int items = n_stab + n + n_pair + n * sc.n_obs;
+  const int items = n_stab + n + n_pair;  // the cube-obstacle pairs follow separately
   for (int it = lane; it < items; it += 32) {
     if (it < n_stab) {  // support i: suffix CoM of the blocks above, in i's yaw frame
       const int i = it;
@@ -209,12 +209,19 @@ __device__ R twin_tower_warp(const TowerScene<R>& sc, const R* rows, R* grad, R*
         my[4 * j + 1] -= gy;
         my[4 * j + 2] -= gz;
       }
-    } else {  // cube vs obstacle sphere
-      const int k = it - n_stab - n - n_pair;
-      const int i = k / sc.n_obs, o = k - i * sc.n_obs;
+    }
+  }
+  // cube-obstacle pairs: G lanes per cube, lane l owns cube l / G and obstacles
+  // o = l % G, l % G + G, ... (register accumulation, one slot update per lane)
+  {
+    const int G = 32 / n;
+    if (lane < n * G) {
+      const int i = lane / G;
+      const R cx = rows[4 * i], cy = rows[4 * i + 1], cz = rows[4 * i + 2];
       R gx = R(0), gy = R(0), gz = R(0);
-      pen_pair_acc<R, true, WG, Q>(rows[4 * i] - sc.ox[o], rows[4 * i + 1] - sc.oy[o], rows[4 * i + 2] - sc.oz[o],
-                                   sc.radius + sc.orad[o], sc.w_c, cost, gx, gy, gz);
+      for (int o = lane - i * G; o < sc.n_obs; o += G)
+        pen_pair_acc<R, true, WG, Q>(cx - sc.ox[o], cy - sc.oy[o], cz - sc.oz[o], sc.radius + sc.orad[o], sc.w_c,
+                                     cost, gx, gy, gz);
       if constexpr (WG) {
         my[4 * i] += gx;
         my[4 * i + 1] += gy;
