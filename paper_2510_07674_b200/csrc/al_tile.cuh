@@ -183,34 +183,10 @@ __device__ __forceinline__ R pen_term(R dx, R dy, R dz, R rsum, bool quad, R* sl
   }
 }
 
-// accumulate one sphere (centre c, radius r) against fixed obstacles: statics + staged
-// spheres [f0, f1); returns the summed value, adds the unscaled gradient to g
-template <typename R>
-__device__ __forceinline__ R pens_fixed(const TrajScene<R>& sc, const R* c, R r, int f0, int f1, bool quad, R* g) {
-  R v = R(0);
-#pragma unroll 4
-  for (int o = 0; o < sc.n_static; ++o) {  // unrolled: overlaps the per-pair MUFU latencies
-    const R dx = c[0] - sc.st_c[o][0], dy = c[1] - sc.st_c[o][1], dz = c[2] - sc.st_c[o][2];
-    R sl;
-    v += pen_term(dx, dy, dz, r + sc.st_r[o], quad, &sl);
-    g[0] -= sl * dx;
-    g[1] -= sl * dy;
-    g[2] -= sl * dz;
-  }
-#pragma unroll 4
-  for (int o = f0; o < f1; ++o) {
-    const R dx = c[0] - sc.staged[o][0], dy = c[1] - sc.staged[o][1], dz = c[2] - sc.staged[o][2];
-    R sl;
-    v += pen_term(dx, dy, dz, r + sc.br[o], quad, &sl);
-    g[0] -= sl * dx;
-    g[1] -= sl * dy;
-    g[2] -= sl * dz;
-  }
-  return v;
-}
-
-// The same for one lane of an 8-lane tile: obstacles o = lane, lane + 8, ... of the
-// combined list (statics, then staged spheres [f0, f1)); the caller tile-sums the results.
+// One sphere (centre c, radius r) against the fixed obstacles -- statics + staged spheres
+// [f0, f1) -- for one lane of an 8-lane tile: obstacles o = lane, lane + 8, ... of the
+// combined list; returns the lane's summed value and adds its unscaled gradient to g (the
+// caller tile-sums both).
 template <typename R>
 __device__ __forceinline__ R pens_fixed_lane(const TrajScene<R>& sc, const R* c, R r, int f0, int f1, bool quad,
                                              int lane, R* g) {
