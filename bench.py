@@ -357,7 +357,10 @@ def run_b200(args):
         "steps": args.steps,
         "warmup": args.warmup,
         "ms_per_step": total_dev / args.steps,
-        "p50_solve_ms": statistics.median(wall_ms),
+        # reference bench.solve_scene span: stage 1 (+ lift + AL), excluding scene load and the
+        # final independent validate (bench.py:190-247); p50_step_ms is the whole timed step
+        "p50_solve_ms": statistics.median(s.time_ms for s in sols),
+        "p50_step_ms": statistics.median(wall_ms),
         "success_rate": succ / args.steps,
         "higher_is_better": True,
         "scaling": "weak",
