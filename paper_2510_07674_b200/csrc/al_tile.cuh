@@ -183,26 +183,34 @@ __device__ __forceinline__ R pen_term(R dx, R dy, R dz, R rsum, bool quad, R* sl
   }
 }
 
-// One sphere (centre c, radius r) against the fixed obstacles -- statics + staged spheres
-// [f0, f1) -- for one lane of an 8-lane tile: obstacles o = lane, lane + 8, ... of the
-// combined list; returns the lane's summed value and adds its unscaled gradient to g (the
-// caller tile-sums both).
+// One sphere against every fixed obstacle (statics, then staged spheres [f0, f1)), on one
+// lane: returns the summed value and adds the unscaled gradient to g.
 template <typename R>
-__device__ __forceinline__ R pens_fixed_lane(const TrajScene<R>& sc, const R* c, R r, int f0, int f1, bool quad,
-                                             int lane, R* g) {
-  R v = R(0);
-  const int ns = sc.n_static, nfix = ns + (f1 - f0);
-#pragma unroll 2
-  for (int o = lane; o < nfix; o += kTile) {
-    const R* oc = o < ns ? sc.st_c[o] : sc.staged[f0 + o - ns];
-    const R orad = o < ns ? sc.st_r[o] : sc.br[f0 + o - ns];
-    const R dx = c[0] - oc[0], dy = c[1] - oc[1], dz = c[2] - oc[2];
+__device__ __forceinline__ R pens_fixed_all(const TrajScene<R>& sc, const R* c, R r, int f0, int f1, bool quad,
+                                            R* g) {
+  const R cx = c[0], cy = c[1], cz = c[2];
+  R v = R(0), gx = R(0), gy = R(0), gz = R(0);
+#pragma unroll 4
+  for (int o = 0; o < sc.n_static; ++o) {
+    const R dx = cx - sc.st_c[o][0], dy = cy - sc.st_c[o][1], dz = cz - sc.st_c[o][2];
     R sl;
-    v += pen_term(dx, dy, dz, r + orad, quad, &sl);
-    g[0] -= sl * dx;
-    g[1] -= sl * dy;
-    g[2] -= sl * dz;
+    v += pen_term(dx, dy, dz, r + sc.st_r[o], quad, &sl);
+    gx -= sl * dx;
+    gy -= sl * dy;
+    gz -= sl * dz;
   }
+#pragma unroll 2
+  for (int o = f0; o < f1; ++o) {
+    const R dx = cx - sc.staged[o][0], dy = cy - sc.staged[o][1], dz = cz - sc.staged[o][2];
+    R sl;
+    v += pen_term(dx, dy, dz, r + sc.br[o], quad, &sl);
+    gx -= sl * dx;
+    gy -= sl * dy;
+    gz -= sl * dz;
+  }
+  g[0] += gx;
+  g[1] += gy;
+  g[2] += gz;
   return v;
 }
 
@@ -265,6 +273,27 @@ __device__ void al_eval(AlCtx<R>& C, const typename TwinSceneOf<R, KIND>::type& 
 #pragma unroll
         for (int c = 0; c < 9; ++c) C.rot[w * 9 + c] = f.Ree[c];
       }
+      if (manip && t == T - 1) {  // placed pose from the final waypoint (trajopt.py:448-472)
+        const R ps = yaw_of(f.Ree) - sc.grasp_yaw;
+        R s, c;
+        Math<R>::sincos_(ps, &s, &c);
+        if (j == 0) {
+          const R ox = sc.grasp_off[0], oy = sc.grasp_off[1], oz = sc.grasp_off[2];
+          C.psi[b] = ps;
+          C.cp[b] = c;
+          C.sp[b] = s;
+          C.rows[4 * b + 0] = f.ee[0] - (c * ox - s * oy);
+          C.rows[4 * b + 1] = f.ee[1] - (s * ox + c * oy);
+          C.rows[4 * b + 2] = f.ee[2] - oz;
+          C.rows[4 * b + 3] = ps;
+        }
+        for (int q = sc.blk_start[b] + j; q < sc.blk_start[b + 1]; q += kTile) {
+          const R ux = sc.bu[q][0], uy = sc.bu[q][1], uz = sc.bu[q][2];
+          C.pl[3 * q + 0] = f.ee[0] + c * ux - s * uy;
+          C.pl[3 * q + 1] = f.ee[1] + s * ux + c * uy;
+          C.pl[3 * q + 2] = f.ee[2] + uz;
+        }
+      }
       if (j < J)
         for (int s = ch.link_start[j]; s < ch.link_start[j + 1]; ++s) tile_sphere(ch, f, s, C.armw + (w * S + s) * 3);
       if (interior) {  // held block = Ree @ FLIP @ u + ee (trajopt.py:441-447)
@@ -306,32 +335,10 @@ __device__ void al_eval(AlCtx<R>& C, const typename TwinSceneOf<R, KIND>::type& 
   __syncthreads();
   C.prof.mark(0);
 
-  // ---------------- P2: aux = placed poses + placement twin; tiles = fixed obstacles ----
+  // ---------------- P2: aux = placement twin (placed poses came from P1); tiles = fixed
+  // obstacles
   if (is_aux) {
     if (manip) {
-      if (lane < B) {
-        const int bb = lane, wf = bb * T + T - 1;
-        const R* Rf = C.rot + wf * 9;
-        const R* ef = C.ee + wf * 3;
-        const R ps = yaw_of(Rf) - sc.grasp_yaw;
-        R s, c;
-        Math<R>::sincos_(ps, &s, &c);
-        C.psi[bb] = ps;
-        C.cp[bb] = c;
-        C.sp[bb] = s;
-        const R ox = sc.grasp_off[0], oy = sc.grasp_off[1], oz = sc.grasp_off[2];
-        C.rows[4 * bb + 0] = ef[0] - (c * ox - s * oy);
-        C.rows[4 * bb + 1] = ef[1] - (s * ox + c * oy);
-        C.rows[4 * bb + 2] = ef[2] - oz;
-        C.rows[4 * bb + 3] = ps;
-        for (int q = sc.blk_start[bb]; q < sc.blk_start[bb + 1]; ++q) {
-          const R ux = sc.bu[q][0], uy = sc.bu[q][1], uz = sc.bu[q][2];
-          C.pl[3 * q + 0] = ef[0] + c * ux - s * uy;
-          C.pl[3 * q + 1] = ef[1] + s * ux + c * uy;
-          C.pl[3 * q + 2] = ef[2] + uz;
-        }
-      }
-      __syncwarp();
       if (C.prof.on && lane == 0) atomicAdd(&g_al_arrive[1][5], (unsigned long long)(clock64() - C.prof.t));
       R cpl = twin_warp<R, KIND, SPB>(tw, C.rows, C.gpose, C.scr, lane, want_grad, pquad);
       if (C.prof.on && lane == 0) atomicAdd(&g_al_arrive[1][6], (unsigned long long)(clock64() - C.prof.t));
@@ -347,42 +354,23 @@ __device__ void al_eval(AlCtx<R>& C, const typename TwinSceneOf<R, KIND>::type& 
       }
     }
   } else if (w < C.L.NW / kTile) {
-    // every sphere of the waypoint against the fixed obstacles, the obstacle list split over
-    // the tile's 8 lanes and tile-summed (the per-lane sphere loop left one lane with all
-    // the held-block pairs on top of its link's spheres). Padding tiles mirror waypoint 0
-    // without writing, so every lane of the tile warps reaches the warp-mask sums.
-    const int wq = is_wp ? w : 0;
-    for (int s = 0; s < S; ++s) {
-      R gg[3] = {R(0), R(0), R(0)};
-      R v = pens_fixed_lane(sc, C.armw + (wq * S + s) * 3, ch.arm_r[s], f0, f1, quad, j, gg);
-      v = tlw.sum(v);
-      gg[0] = tlw.sum(gg[0]);
-      gg[1] = tlw.sum(gg[1]);
-      gg[2] = tlw.sum(gg[2]);
-      if (is_wp && j == 0) {
-        carm += v;
-        R* ga = C.ga + (w * S + s) * 3;
-        ga[0] = gg[0];
-        ga[1] = gg[1];
-        ga[2] = gg[2];
-      }
-    }
-    if (manip) {  // held-block spheres: uniform bound SB over the warp, inactive slots add zero
-      for (int s = 0; s < SBn; ++s) {
-        const bool act = interior && s < nh;
+    // Sphere-major: the tile's 8 lanes take the waypoint's spheres (arm spheres, then the
+    // held-block spheres) round-robin, each against the whole fixed list, so a sphere's
+    // gradient stays lane-local (no tile sums) and the values join the warp sums of P3.
+    if (is_wp) {
+      const int n_items = S + (interior ? nh : 0);
+      for (int it = j; it < n_items; it += kTile) {
+        const bool arm = it < S;
+        const int s = arm ? it : it - S;
+        const R* c = arm ? C.armw + (w * S + s) * 3 : C.hp + (w * SBn + s) * 3;
         R gg[3] = {R(0), R(0), R(0)};
-        R v = act ? pens_fixed_lane(sc, C.hp + (w * SBn + s) * 3, sc.br[h0 + s], f0, f1, quad, j, gg) : R(0);
-        v = tlw.sum(v);
-        gg[0] = tlw.sum(gg[0]);
-        gg[1] = tlw.sum(gg[1]);
-        gg[2] = tlw.sum(gg[2]);
-        if (act && j == 0) {
-          cblk += v;
-          R* gh = C.gh + (w * SBn + s) * 3;
-          gh[0] = gg[0];
-          gh[1] = gg[1];
-          gh[2] = gg[2];
-        }
+        const R v = pens_fixed_all(sc, c, arm ? ch.arm_r[s] : sc.br[h0 + s], f0, f1, quad, gg);
+        R* go = arm ? C.ga + (w * S + s) * 3 : C.gh + (w * SBn + s) * 3;
+        go[0] = gg[0];
+        go[1] = gg[1];
+        go[2] = gg[2];
+        if (arm) carm += v;
+        else cblk += v;
       }
     }
   }
@@ -554,8 +542,17 @@ __device__ void al_eval(AlCtx<R>& C, const typename TwinSceneOf<R, KIND>::type& 
   if (want_grad && manip && is_aux) {
     for (int it = lane; it < 8 * B; it += 32) {
       const int cls = it / (4 * B), jb = (it / 4) % B, i = it % 4;
+      // waypoint order kept; 8 loads issued before their (sequential) adds
       R s = R(0);
-      for (int wv = (jb + 1) * T; wv < W; ++wv) s += C.pg[((wv * 2 + cls) * B + jb) * 4 + i];
+      int wv = (jb + 1) * T;
+      for (; wv + 8 <= W; wv += 8) {
+        R v[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) v[k] = C.pg[(((wv + k) * 2 + cls) * B + jb) * 4 + i];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) s += v[k];
+      }
+      for (; wv < W; ++wv) s += C.pg[((wv * 2 + cls) * B + jb) * 4 + i];
       C.pgsum[it] = s;
     }
   }

@@ -156,7 +156,13 @@ template <typename R>
 __device__ __forceinline__ R wrap_yaw(R a) {
   const R two_pi = R(6.283185307179586476925286766559);
   const R pi = R(3.1415926535897932384626433832795);
-  R w = fmod(a + pi, two_pi);
+  // x in (-2m, 2m) (every yaw difference here): fmod is x, x - m or x + m, each exact
+  // (Sterbenz), so the branch gives fmod's bits without its loop (fmod(-m, m) = -0 vs
+  // +0 here: both fail the w < 0 test below, same result)
+  const R x = a + pi;
+  R w = (x > -R(2) * two_pi && x < R(2) * two_pi)
+            ? (x >= two_pi ? x - two_pi : (x <= -two_pi ? x + two_pi : x))
+            : fmod(x, two_pi);
   if (w < R(0)) w += two_pi;
   w -= pi;
   if (w <= -pi) w += two_pi;

@@ -68,8 +68,11 @@ __device__ __forceinline__ void lift_target(const TrajScene<R>& sc, const double
 // one CTA per (draw, target) group; one 8-lane tile per seeded restart (lane = joint), each
 // tile in its own warp (lanes 8-31 idle) so that restarts in different phases (IK vs
 // speculative polish) never share a warp and serialise on divergence
-template <typename R>
-__global__ void __launch_bounds__(1024) k_ik_group(const TrajScene<R>* __restrict__ g_scene, int n_targets, int n_draws,
+// MAXT = the block-size bound: 512 (<= 16 restarts) lets ptxas use 128 registers (the
+// per-iteration FK/DLS state spills under the 64-register cap of 1024-thread blocks); the
+// launcher takes it when the grid fits one CTA per SM.
+template <typename R, int MAXT>
+__global__ void __launch_bounds__(MAXT) k_ik_group(const TrajScene<R>* __restrict__ g_scene, int n_targets, int n_draws,
                                                   uint64_t seed, uint64_t draw_stride, int restarts, int max_iters,
                                                   double damping, const double* __restrict__ tpos_in,
                                                   const double* __restrict__ tyaw_in, const double* __restrict__ rows,
