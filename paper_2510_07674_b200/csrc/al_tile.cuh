@@ -430,15 +430,10 @@ __device__ void al_eval(AlCtx<R>& C, const typename TwinSceneOf<R, KIND>::type& 
             }
           }
         }
-        if (want_grad) {  // tile-reduce, lane 0 stores [class][block jb][G xyz | G yaw]
-#pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            const R av = tlw.sum(A[i]), hv = tlw.sum(H[i]);
-            if (act && j == 0) {
-              C.pg[((w * 2 + 0) * B + jb) * 4 + i] = av;
-              C.pg[((w * 2 + 1) * B + jb) * 4 + i] = hv;
-            }
-          }
+        if (want_grad) {  // tile reduce-scatter: lane j stores [class j/4][block jb][G xyz | G yaw][j%4]
+          const R v8[8] = {A[0], A[1], A[2], A[3], H[0], H[1], H[2], H[3]};
+          const R r = tlw.sum8_scatter(v8);
+          if (act) C.pg[((w * 2 + (j >> 2)) * B + jb) * 4 + (j & 3)] = r;
         }
       }
     }

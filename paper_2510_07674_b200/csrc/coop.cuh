@@ -55,6 +55,18 @@ struct Tile {
     v += xr(v, 4);
     return v;
   }
+  // Reduce-scatter of 8 per-lane values: lane j returns the tile sum of v[j] (3 levels,
+  // 4 + 2 + 1 shuffles instead of 8 x 3); each sum is formed on one lane only.
+  template <typename R>
+  __device__ __forceinline__ R sum8_scatter(const R (&v)[8]) const {
+    const bool h2 = (j & 4) != 0, h1 = (j & 2) != 0, h0 = (j & 1) != 0;
+    R a[4], b[2];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) a[k] = (h2 ? v[k + 4] : v[k]) + xr(h2 ? v[k] : v[k + 4], 4);
+#pragma unroll
+    for (int k = 0; k < 2; ++k) b[k] = (h1 ? a[k + 2] : a[k]) + xr(h1 ? a[k] : a[k + 2], 2);
+    return (h0 ? b[1] : b[0]) + xr(h0 ? b[0] : b[1], 1);
+  }
   template <typename R>
   __device__ __forceinline__ R max(R v) const {
     v = fmax(v, xr(v, 1));

@@ -178,13 +178,19 @@ __device__ R twin_tower_warp(const TowerScene<R>& sc, const R* rows, R* grad, R*
         const R glx = factor * ux, gly = factor * uy;
         const R gwx = c * glx - s * gly, gwy = s * glx + c * gly;
         const R drx = -s * relx + c * rely, dry = -c * relx - s * rely;
-        my[4 * i + 3] += glx * drx + gly * dry;
+        // slot updates as load-all / store-all (distinct slots; the shared-memory RMWs
+        // otherwise serialise on possible aliasing)
+        R* mi = my + 4 * i;
+        const R m0 = mi[0], m1 = mi[1], m3 = mi[3];
+        mi[3] = m3 + (glx * drx + gly * dry);
+        mi[0] = m0 - gwx;
+        mi[1] = m1 - gwy;
+        const R ax = gwx / cnt, ay = gwy / cnt;
         for (int k = i + 1; k < n; ++k) {
-          my[4 * k] += gwx / cnt;
-          my[4 * k + 1] += gwy / cnt;
+          const R mx = my[4 * k], myy = my[4 * k + 1];
+          my[4 * k] = mx + ax;
+          my[4 * k + 1] = myy + ay;
         }
-        my[4 * i] -= gwx;
-        my[4 * i + 1] -= gwy;
       }
     } else if (it < n_stab + n) {  // height target (i+1) * side
       const int i = it - n_stab;
@@ -202,12 +208,15 @@ __device__ R twin_tower_warp(const TowerScene<R>& sc, const R* rows, R* grad, R*
       pen_pair_acc<R, true, WG, Q>(rows[4 * i] - rows[4 * j], rows[4 * i + 1] - rows[4 * j + 1],
                                    rows[4 * i + 2] - rows[4 * j + 2], sc.side, sc.w_c, cost, gx, gy, gz);
       if constexpr (WG) {
-        my[4 * i] += gx;
-        my[4 * i + 1] += gy;
-        my[4 * i + 2] += gz;
-        my[4 * j] -= gx;
-        my[4 * j + 1] -= gy;
-        my[4 * j + 2] -= gz;
+        R* mi = my + 4 * i;
+        R* mj = my + 4 * j;
+        const R a0 = mi[0], a1 = mi[1], a2 = mi[2], b0 = mj[0], b1 = mj[1], b2 = mj[2];
+        mi[0] = a0 + gx;
+        mi[1] = a1 + gy;
+        mi[2] = a2 + gz;
+        mj[0] = b0 - gx;
+        mj[1] = b1 - gy;
+        mj[2] = b2 - gz;
       }
     }
   }
@@ -223,9 +232,11 @@ __device__ R twin_tower_warp(const TowerScene<R>& sc, const R* rows, R* grad, R*
         pen_pair_acc<R, true, WG, Q>(cx - sc.ox[o], cy - sc.oy[o], cz - sc.oz[o], sc.radius + sc.orad[o], sc.w_c,
                                      cost, gx, gy, gz);
       if constexpr (WG) {
-        my[4 * i] += gx;
-        my[4 * i + 1] += gy;
-        my[4 * i + 2] += gz;
+        R* mi = my + 4 * i;
+        const R a0 = mi[0], a1 = mi[1], a2 = mi[2];
+        mi[0] = a0 + gx;
+        mi[1] = a1 + gy;
+        mi[2] = a2 + gz;
       }
     }
   }
