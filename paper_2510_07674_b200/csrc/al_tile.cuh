@@ -534,21 +534,25 @@ __device__ void al_eval(AlCtx<R>& C, const typename TwinSceneOf<R, KIND>::type& 
     C.scal[kSc1] = (l1 + mu * c1) * R(prm.w_arm);
     C.scal[kSc2] = (l2 + mu * c2) * R(prm.w_block);
   }
-  if (want_grad && manip && is_aux) {
-    for (int it = lane; it < 8 * B; it += 32) {
-      const int cls = it / (4 * B), jb = (it / 4) % B, i = it % 4;
-      // waypoint order kept; 8 loads issued before their (sequential) adds
-      R s = R(0);
-      int wv = (jb + 1) * T;
-      for (; wv + 8 <= W; wv += 8) {
-        R v[8];
-#pragma unroll
-        for (int k = 0; k < 8; ++k) v[k] = C.pg[(((wv + k) * 2 + cls) * B + jb) * 4 + i];
-#pragma unroll
-        for (int k = 0; k < 8; ++k) s += v[k];
+  // placed-block partials summed over the later segments' waypoints (waypoint order per
+  // quarter, quarters combined (q0 + q1) + (q2 + q3)): 4 lanes per item on the tile warps
+  // other than warp 0 (thread 0 forms the totals above); the aux warp when there is none
+  if (want_grad && manip) {
+    const int total = 32 * B;  // 8B items x 4 quarters
+    const bool tiles = C.L.NW >= 64;
+    if (tiles ? (!is_aux && tid >= 32) : is_aux) {
+      const int first = tiles ? ((tid - 32) & ~31) : 0, stride = tiles ? C.L.NW - 32 : 32;
+      for (int u0 = first; u0 < total; u0 += stride) {  // warp-uniform trip count
+        const int u = u0 + lane, it = u >> 2, part = u & 3;
+        R s = R(0);
+        if (u < total) {
+          const int cls = it / (4 * B), jb = (it / 4) % B, i = it % 4;
+          for (int wv = (jb + 1) * T + part; wv < W; wv += 4) s += C.pg[((wv * 2 + cls) * B + jb) * 4 + i];
+        }
+        s += __shfl_xor_sync(0xffffffffu, s, 1);
+        s += __shfl_xor_sync(0xffffffffu, s, 2);
+        if (u < total && part == 0) C.pgsum[it] = s;
       }
-      for (; wv < W; ++wv) s += C.pg[((wv * 2 + cls) * B + jb) * 4 + i];
-      C.pgsum[it] = s;
     }
   }
   C.prof.arrive(3, C.L.NW);
