@@ -252,7 +252,7 @@ __device__ void al_eval(AlCtx<R>& C, const typename TwinSceneOf<R, KIND>::type& 
   WpState<R> st;
   R obj_w = R(0), carm = R(0), cblk = R(0);
 
-  // ---------------- P1: tile FK, sphere centres, leg, start terms ------------------------
+  // ---------------- P1: tile FK, sphere centres, placed poses ----------------------------
   if (!is_aux && w < C.L.NW / kTile) {
     const int wq = is_wp ? w : 0;  // padding tiles mirror waypoint 0 (no writes)
     const R qj = j < J ? C.x[wq * kXS + j] : R(0);
@@ -306,30 +306,6 @@ __device__ void al_eval(AlCtx<R>& C, const typename TwinSceneOf<R, KIND>::type& 
         }
       }
     }
-    // path length (trajopt.py:474-476): tile sum of the leg's squared components
-    R dv = R(0);
-    if (is_wp && t < T - 1 && j < J) dv = C.x[(wq + 1) * kXS + j] - qj;
-    const R s2 = tlw.sum(dv * dv);
-    if (is_wp && t < T - 1) {
-      const R ln = Math<R>::sqrt_(s2);
-      if (j == 0) obj_w += ln;
-      C.unit[w * kXS + j] = (ln > R(1e-12) && j < J) ? dv / ln : R(0);
-    }
-    // start alignment (trajopt.py:477-494), uniform across the tile
-    if (is_wp && manip && t == 0) {
-      st.d0[0] = f.ee[0] - sc.pick_pos[b][0];
-      st.d0[1] = f.ee[1] - sc.pick_pos[b][1];
-      st.d0[2] = f.ee[2] - sc.pick_pos[b][2];
-      R cosd = -f.Ree[8];
-      cosd = cosd < R(-1) ? R(-1) : (cosd > R(1) ? R(1) : cosd);
-      const R th = Math<R>::acos_(cosd);
-      st.dy0 = wrap_yaw(yaw_of(f.Ree) - sc.pick_yaw[b]);
-      const R sth = Math<R>::sqrt_(fmax(R(1) - cosd * cosd, R(0)));
-      st.fac = sth > R(1e-8) ? R(-2) * th / fmax(sth, R(1e-8)) : (cosd > R(0) ? R(-2) : R(0));
-      if (j == 0)
-        obj_w += w_start * ((((st.d0[0] * st.d0[0] + st.d0[1] * st.d0[1]) + st.d0[2] * st.d0[2]) + th * th) +
-                            st.dy0 * st.dy0);
-    }
   }
   C.prof.arrive(0, C.L.NW);
   __syncthreads();
@@ -354,6 +330,34 @@ __device__ void al_eval(AlCtx<R>& C, const typename TwinSceneOf<R, KIND>::type& 
       }
     }
   } else if (w < C.L.NW / kTile) {
+    // path length and start alignment moved here from P1: the tile warps have slack in P2
+    // (the aux warp's placement twin bounds it), so P1 ends sooner
+    const int wq = is_wp ? w : 0;
+    const R qj = j < J ? C.x[wq * kXS + j] : R(0);
+    // path length (trajopt.py:474-476): tile sum of the leg's squared components
+    R dv = R(0);
+    if (is_wp && t < T - 1 && j < J) dv = C.x[(wq + 1) * kXS + j] - qj;
+    const R s2 = tlw.sum(dv * dv);
+    if (is_wp && t < T - 1) {
+      const R ln = Math<R>::sqrt_(s2);
+      if (j == 0) obj_w += ln;
+      C.unit[w * kXS + j] = (ln > R(1e-12) && j < J) ? dv / ln : R(0);
+    }
+    // start alignment (trajopt.py:477-494), uniform across the tile
+    if (is_wp && manip && t == 0) {
+      st.d0[0] = st.ee[0] - sc.pick_pos[b][0];
+      st.d0[1] = st.ee[1] - sc.pick_pos[b][1];
+      st.d0[2] = st.ee[2] - sc.pick_pos[b][2];
+      R cosd = -st.Ree[8];
+      cosd = cosd < R(-1) ? R(-1) : (cosd > R(1) ? R(1) : cosd);
+      const R th = Math<R>::acos_(cosd);
+      st.dy0 = wrap_yaw(yaw_of(st.Ree) - sc.pick_yaw[b]);
+      const R sth = Math<R>::sqrt_(fmax(R(1) - cosd * cosd, R(0)));
+      st.fac = sth > R(1e-8) ? R(-2) * th / fmax(sth, R(1e-8)) : (cosd > R(0) ? R(-2) : R(0));
+      if (j == 0)
+        obj_w += w_start * ((((st.d0[0] * st.d0[0] + st.d0[1] * st.d0[1]) + st.d0[2] * st.d0[2]) + th * th) +
+                            st.dy0 * st.dy0);
+    }
     // Sphere-major: the tile's 8 lanes take the waypoint's spheres (arm spheres, then the
     // held-block spheres) round-robin, each against the whole fixed list, so a sphere's
     // gradient stays lane-local (no tile sums) and the values join the warp sums of P3.
