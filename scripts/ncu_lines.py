@@ -18,8 +18,11 @@ for r in csv.reader(io.StringIO(out)):
     elif len(r) >= 3 and r[0] == "Line No":
         hdr = r
     elif hdr and r and r[0].isdigit():
-        s = int(r[4] or 0) if r[4] not in ("", "-") else 0
-        e = int(r[7] or 0) if r[7] not in ("", "-") else 0
+        try:
+            s = int(r[4] or 0) if r[4] not in ("", "-") else 0
+            e = int(r[7] or 0) if r[7] not in ("", "-") else 0
+        except ValueError:  # a source line whose text spilled into the numeric columns
+            continue
         lines.append((s, e, cur, int(r[0]), r[1].strip()[:100]))
 tot = sum(x[0] for x in lines) or 1
 byfile = {}
