@@ -316,7 +316,7 @@ __device__ void al_eval(AlCtx<R>& C, const typename TwinSceneOf<R, KIND>::type& 
   if (is_aux) {
     if (manip) {
       if (C.prof.on && lane == 0) atomicAdd(&g_al_arrive[1][5], (unsigned long long)(clock64() - C.prof.t));
-      R cpl = twin_warp<R, KIND, SPB>(tw, C.rows, C.gpose, C.scr, lane, want_grad, pquad);
+      R cpl = twin_warp<R, KIND, SPB>(tw, C.rows, C.gpose, C.scr, lane, want_grad, pquad, KIND == 2);
       if (C.prof.on && lane == 0) atomicAdd(&g_al_arrive[1][6], (unsigned long long)(clock64() - C.prof.t));
       if (lane == 0) {
         if (sc.anchor) {
@@ -330,6 +330,11 @@ __device__ void al_eval(AlCtx<R>& C, const typename TwinSceneOf<R, KIND>::type& 
       }
     }
   } else if (w < C.L.NW / kTile) {
+    // tower scenes: the last tile warp runs the twin's cube-obstacle pairs first, handing
+    // them to the aux warp at named barrier 1 (the twin bounds this phase)
+    if constexpr (KIND == 2) {
+      if (manip && (tid >> 5) == C.L.NW / 32 - 1) twin_tower_obstacles_ext<R>(tw, C.rows, C.scr, lane, want_grad, pquad);
+    }
     // path length and start alignment moved here from P1: the tile warps have slack in P2
     // (the aux warp's placement twin bounds it), so P1 ends sooner
     const int wq = is_wp ? w : 0;

@@ -17,7 +17,14 @@
 namespace spasm {
 
 // scratch (elements of R) the warp twin needs for n bodies
-__host__ __device__ inline int twin_warp_scratch(int n) { return 2 * n + 32 * 4 * n + 2; }
+// (64 slot rows: the tower twin's cube-obstacle pairs may run on a second warp, rows 32-63,
+// with its cost at the end)
+__host__ __device__ inline int twin_warp_scratch(int n) { return 2 * n + 64 * 4 * n + 3; }
+
+// named barrier 1 between the aux warp (sync) and the tile warp that computes the tower
+// twin's cube-obstacle pairs (arrive); 64 threads, both warps converged
+__device__ __forceinline__ void twin_ext_arrive() { asm volatile("bar.arrive 1, 64;" ::: "memory"); }
+__device__ __forceinline__ void twin_ext_sync() { asm volatile("bar.sync 1, 64;" ::: "memory"); }
 
 template <typename R>
 __device__ __forceinline__ R warp_sum_fixed(R v) {
@@ -27,15 +34,15 @@ __device__ __forceinline__ R warp_sum_fixed(R v) {
 }
 
 template <typename R, bool WG>
-__device__ __forceinline__ void twin_reduce_slots(const R* slots, int nv, R* grad, int lane) {
+__device__ __forceinline__ void twin_reduce_slots(const R* slots, int nv, R* grad, int lane, int rows = 32) {
   if constexpr (WG) {
     __syncwarp();
     for (int k = lane; k < nv; k += 32) {
       // 4 interleaved partial sums (fixed order): the 32 loads issue back to back instead
       // of one dependent load-add chain
       R s0 = R(0), s1 = R(0), s2 = R(0), s3 = R(0);
-#pragma unroll
-      for (int l = 0; l < 32; l += 4) {
+#pragma unroll 8
+      for (int l = 0; l < rows; l += 4) {
         s0 += slots[l * nv + k];
         s1 += slots[(l + 1) * nv + k];
         s2 += slots[(l + 2) * nv + k];
@@ -141,8 +148,55 @@ __device__ R twin_tetris_warp(const TetrisScene<R>& sc, const R* rows, R* grad, 
 }
 
 // ---- tower (free yaw; rows (x, y, z, yaw) per block) ------------------------------------
+// cube-obstacle pairs: G lanes per cube, lane l owns cube l / G and obstacles
+// o = l % G, l % G + G, ... (register accumulation, one slot update per lane)
 template <typename R, bool WG, bool Q>
-__device__ R twin_tower_warp(const TowerScene<R>& sc, const R* rows, R* grad, R* scr, int lane) {
+__device__ __forceinline__ void twin_tower_obstacles(const TowerScene<R>& sc, const R* rows, R* my, int lane,
+                                                     R& cost) {
+  const int n = sc.n_blocks;
+  const int G = 32 / n;
+  if (lane < n * G) {
+    const int i = lane / G;
+    const R cx = rows[4 * i], cy = rows[4 * i + 1], cz = rows[4 * i + 2];
+    R gx = R(0), gy = R(0), gz = R(0);
+    for (int o = lane - i * G; o < sc.n_obs; o += G)
+      pen_pair_acc<R, true, WG, Q>(cx - sc.ox[o], cy - sc.oy[o], cz - sc.oz[o], sc.radius + sc.orad[o], sc.w_c,
+                                   cost, gx, gy, gz);
+    if constexpr (WG) {
+      R* mi = my + 4 * i;
+      const R a0 = mi[0], a1 = mi[1], a2 = mi[2];
+      mi[0] = a0 + gx;
+      mi[1] = a1 + gy;
+      mi[2] = a2 + gz;
+    }
+  }
+}
+
+// The cube-obstacle pairs on another (full, converged) warp of the CTA: its lanes fill slot
+// rows 32-63 and the pairs' cost, then arrive on named barrier 1; the aux warp's
+// twin_tower_warp(ext = true) syncs there before its slot reduction.
+template <typename R>
+__device__ void twin_tower_obstacles_ext(const TowerScene<R>& sc, const R* rows, R* scr, int lane, bool want_grad,
+                                         bool quad) {
+  const int n = sc.n_blocks, nv = 4 * n;
+  R* my = scr + 2 * n + (32 + lane) * nv;
+  R cost = R(0);
+  if (want_grad) {
+    for (int k = 0; k < nv; ++k) my[k] = R(0);
+    if (quad) twin_tower_obstacles<R, true, true>(sc, rows, my, lane, cost);
+    else twin_tower_obstacles<R, true, false>(sc, rows, my, lane, cost);
+  } else {
+    if (quad) twin_tower_obstacles<R, false, true>(sc, rows, my, lane, cost);
+    else twin_tower_obstacles<R, false, false>(sc, rows, my, lane, cost);
+  }
+  cost = warp_sum_fixed(cost);
+  if (lane == 0) scr[2 * n + 64 * nv] = cost;
+  __syncwarp();
+  twin_ext_arrive();
+}
+
+template <typename R, bool WG, bool Q>
+__device__ R twin_tower_warp(const TowerScene<R>& sc, const R* rows, R* grad, R* scr, int lane, bool ext = false) {
   const int n = sc.n_blocks;
   const int nv = 4 * n;
   R* gl = scr + 2 * n;
@@ -220,28 +274,13 @@ __device__ R twin_tower_warp(const TowerScene<R>& sc, const R* rows, R* grad, R*
       }
     }
   }
-  // cube-obstacle pairs: G lanes per cube, lane l owns cube l / G and obstacles
-  // o = l % G, l % G + G, ... (register accumulation, one slot update per lane)
-  {
-    const int G = 32 / n;
-    if (lane < n * G) {
-      const int i = lane / G;
-      const R cx = rows[4 * i], cy = rows[4 * i + 1], cz = rows[4 * i + 2];
-      R gx = R(0), gy = R(0), gz = R(0);
-      for (int o = lane - i * G; o < sc.n_obs; o += G)
-        pen_pair_acc<R, true, WG, Q>(cx - sc.ox[o], cy - sc.oy[o], cz - sc.oz[o], sc.radius + sc.orad[o], sc.w_c,
-                                     cost, gx, gy, gz);
-      if constexpr (WG) {
-        R* mi = my + 4 * i;
-        const R a0 = mi[0], a1 = mi[1], a2 = mi[2];
-        mi[0] = a0 + gx;
-        mi[1] = a1 + gy;
-        mi[2] = a2 + gz;
-      }
-    }
-  }
+  if (!ext) twin_tower_obstacles<R, WG, Q>(sc, rows, my, lane, cost);
   cost = warp_sum_fixed(cost);
-  twin_reduce_slots<R, WG>(gl, nv, grad, lane);
+  if (ext) {
+    twin_ext_sync();
+    cost += scr[2 * n + 64 * nv];
+  }
+  twin_reduce_slots<R, WG>(gl, nv, grad, lane, ext ? 64 : 32);
   __syncwarp();
   return cost;
 }
@@ -249,7 +288,8 @@ __device__ R twin_tower_warp(const TowerScene<R>& sc, const R* rows, R* grad, R*
 // Cost of the placement twin on all 32 lanes of the calling warp; grad (4 per body)
 // written when want_grad.
 template <typename R, int KIND, int SPB, class TS>
-__device__ R twin_warp(const TS& ts, const R* rows, R* grad, R* scr, int lane, bool want_grad, bool quad) {
+__device__ R twin_warp(const TS& ts, const R* rows, R* grad, R* scr, int lane, bool want_grad, bool quad,
+                      bool ext = false) {
   if constexpr (KIND == 1) {
     if (want_grad)
       return quad ? twin_tetris_warp<R, SPB, true, true>(ts, rows, grad, scr, lane)
@@ -258,10 +298,10 @@ __device__ R twin_warp(const TS& ts, const R* rows, R* grad, R* scr, int lane, b
                 : twin_tetris_warp<R, SPB, false, false>(ts, rows, grad, scr, lane);
   } else if constexpr (KIND == 2) {
     if (want_grad)
-      return quad ? twin_tower_warp<R, true, true>(ts, rows, grad, scr, lane)
-                  : twin_tower_warp<R, true, false>(ts, rows, grad, scr, lane);
-    return quad ? twin_tower_warp<R, false, true>(ts, rows, grad, scr, lane)
-                : twin_tower_warp<R, false, false>(ts, rows, grad, scr, lane);
+      return quad ? twin_tower_warp<R, true, true>(ts, rows, grad, scr, lane, ext)
+                  : twin_tower_warp<R, true, false>(ts, rows, grad, scr, lane, ext);
+    return quad ? twin_tower_warp<R, false, true>(ts, rows, grad, scr, lane, ext)
+                : twin_tower_warp<R, false, false>(ts, rows, grad, scr, lane, ext);
   } else {
     return R(0);
   }
