@@ -251,6 +251,9 @@ __device__ void al_eval(AlCtx<R>& C, const typename TwinSceneOf<R, KIND>::type& 
   const R w_start = R(prm.w_start);
   WpState<R> st;
   R obj_w = R(0), carm = R(0), cblk = R(0);
+  // tower twin helpers (twin_warp.cuh): the last tile warp takes the cube-obstacle pairs,
+  // the one before it the stability supports
+  const int twin_ext = KIND == 2 ? (C.L.NW >= 64 ? 2 : 1) : 0;
 
   // ---------------- P1: tile FK, sphere centres, placed poses ----------------------------
   if (!is_aux && w < C.L.NW / kTile) {
@@ -316,7 +319,7 @@ __device__ void al_eval(AlCtx<R>& C, const typename TwinSceneOf<R, KIND>::type& 
   if (is_aux) {
     if (manip) {
       if (C.prof.on && lane == 0) atomicAdd(&g_al_arrive[1][5], (unsigned long long)(clock64() - C.prof.t));
-      R cpl = twin_warp<R, KIND, SPB>(tw, C.rows, C.gpose, C.scr, lane, want_grad, pquad, KIND == 2);
+      R cpl = twin_warp<R, KIND, SPB>(tw, C.rows, C.gpose, C.scr, lane, want_grad, pquad, twin_ext);
       if (C.prof.on && lane == 0) atomicAdd(&g_al_arrive[1][6], (unsigned long long)(clock64() - C.prof.t));
       if (lane == 0) {
         if (sc.anchor) {
@@ -330,10 +333,11 @@ __device__ void al_eval(AlCtx<R>& C, const typename TwinSceneOf<R, KIND>::type& 
       }
     }
   } else if (w < C.L.NW / kTile) {
-    // tower scenes: the last tile warp runs the twin's cube-obstacle pairs first, handing
-    // them to the aux warp at named barrier 1 (the twin bounds this phase)
+    // tower scenes: the last tile warps run parts of the twin first, handing them to the
+    // aux warp at named barrier 1 (the twin bounds this phase)
     if constexpr (KIND == 2) {
-      if (manip && (tid >> 5) == C.L.NW / 32 - 1) twin_tower_obstacles_ext<R>(tw, C.rows, C.scr, lane, want_grad, pquad);
+      const int part = C.L.NW / 32 - (tid >> 5);  // 1 = last tile warp, 2 = the one before
+      if (manip && part <= twin_ext) twin_tower_helper<R>(tw, C.rows, C.scr, lane, want_grad, pquad, part, twin_ext);
     }
     // path length and start alignment moved here from P1: the tile warps have slack in P2
     // (the aux warp's placement twin bounds it), so P1 ends sooner

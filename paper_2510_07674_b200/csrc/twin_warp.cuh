@@ -17,14 +17,13 @@
 namespace spasm {
 
 // scratch (elements of R) the warp twin needs for n bodies
-// (64 slot rows: the tower twin's cube-obstacle pairs may run on a second warp, rows 32-63,
-// with its cost at the end)
-__host__ __device__ inline int twin_warp_scratch(int n) { return 2 * n + 64 * 4 * n + 3; }
+// (96 slot rows: the tower twin may hand parts to two helper warps, twin_tower_helper)
+__host__ __device__ inline int twin_warp_scratch(int n) { return 2 * n + 96 * 4 * n + 4; }
 
-// named barrier 1 between the aux warp (sync) and the tile warp that computes the tower
-// twin's cube-obstacle pairs (arrive); 64 threads, both warps converged
-__device__ __forceinline__ void twin_ext_arrive() { asm volatile("bar.arrive 1, 64;" ::: "memory"); }
-__device__ __forceinline__ void twin_ext_sync() { asm volatile("bar.sync 1, 64;" ::: "memory"); }
+// named barrier 1 between the aux warp (sync) and the tile warps that compute parts of the
+// tower twin (arrive); 32 threads per warp, every warp converged
+__device__ __forceinline__ void twin_ext_arrive(int count) { asm volatile("bar.arrive 1, %0;" ::"r"(count) : "memory"); }
+__device__ __forceinline__ void twin_ext_sync(int count) { asm volatile("bar.sync 1, %0;" ::"r"(count) : "memory"); }
 
 template <typename R>
 __device__ __forceinline__ R warp_sum_fixed(R v) {
@@ -172,41 +171,25 @@ __device__ __forceinline__ void twin_tower_obstacles(const TowerScene<R>& sc, co
   }
 }
 
-// The cube-obstacle pairs on another (full, converged) warp of the CTA: its lanes fill slot
-// rows 32-63 and the pairs' cost, then arrive on named barrier 1; the aux warp's
-// twin_tower_warp(ext = true) syncs there before its slot reduction.
-template <typename R>
-__device__ void twin_tower_obstacles_ext(const TowerScene<R>& sc, const R* rows, R* scr, int lane, bool want_grad,
-                                         bool quad) {
-  const int n = sc.n_blocks, nv = 4 * n;
-  R* my = scr + 2 * n + (32 + lane) * nv;
-  R cost = R(0);
-  if (want_grad) {
-    for (int k = 0; k < nv; ++k) my[k] = R(0);
-    if (quad) twin_tower_obstacles<R, true, true>(sc, rows, my, lane, cost);
-    else twin_tower_obstacles<R, true, false>(sc, rows, my, lane, cost);
-  } else {
-    if (quad) twin_tower_obstacles<R, false, true>(sc, rows, my, lane, cost);
-    else twin_tower_obstacles<R, false, false>(sc, rows, my, lane, cost);
-  }
-  cost = warp_sum_fixed(cost);
-  if (lane == 0) scr[2 * n + 64 * nv] = cost;
-  __syncwarp();
-  twin_ext_arrive();
-}
+// Slot rows of the tower twin's work split: rows 0-31 the aux warp (pairs, heights and,
+// without helpers, everything), rows 32-63 the cube-obstacle pairs, rows 64-95 the
+// stability supports, each helper on a tile warp; helper costs follow the 96 rows.
+__host__ __device__ inline int twin_ext_count(int ext) { return 32 * (1 + ext); }
 
+// Items [it_lo, it_hi) of the tower twin (supports i < B-1, heights, cube pairs) and, when
+// `obstacles`, the cube-obstacle pairs, accumulated into this lane's slot row `my` (zeroed
+// here); returns the lane's cost.
 template <typename R, bool WG, bool Q>
-__device__ R twin_tower_warp(const TowerScene<R>& sc, const R* rows, R* grad, R* scr, int lane, bool ext = false) {
+__device__ R twin_tower_core(const TowerScene<R>& sc, const R* rows, R* my, int lane, int it_lo, int it_hi,
+                             bool obstacles) {
   const int n = sc.n_blocks;
   const int nv = 4 * n;
-  R* gl = scr + 2 * n;
-  R* my = gl + lane * nv;
   if constexpr (WG)
     for (int k = 0; k < nv; ++k) my[k] = R(0);
   R cost = R(0);
   const int n_stab = n - 1, n_pair = n * (n - 1) / 2;
   const int items = n_stab + n + n_pair;  // the cube-obstacle pairs follow separately
-  for (int it = lane; it < items; it += 32) {
+  for (int it = it_lo + lane; it < (it_hi < items ? it_hi : items); it += 32) {
     if (it < n_stab) {  // support i: suffix CoM of the blocks above, in i's yaw frame
       const int i = it;
       R sxs = R(0), sys = R(0);
@@ -274,13 +257,48 @@ __device__ R twin_tower_warp(const TowerScene<R>& sc, const R* rows, R* grad, R*
       }
     }
   }
-  if (!ext) twin_tower_obstacles<R, WG, Q>(sc, rows, my, lane, cost);
+  if (obstacles) twin_tower_obstacles<R, WG, Q>(sc, rows, my, lane, cost);
+  return cost;
+}
+
+// One helper warp of the tower twin (part 1 = cube-obstacle pairs, 2 = stability supports):
+// fills its slot rows and cost, then arrives on named barrier 1 where the aux warp's
+// twin_tower_warp(ext) waits. The warp must be full and converged.
+template <typename R>
+__device__ void twin_tower_helper(const TowerScene<R>& sc, const R* rows, R* scr, int lane, bool want_grad, bool quad,
+                                  int part, int ext) {
+  const int n = sc.n_blocks, nv = 4 * n;
+  R* my = scr + 2 * n + (32 * part + lane) * nv;
+  const int lo = 0, hi = part == 2 ? n - 1 : 0;
+  const bool obs = part == 1;
+  R cost;
+  if (want_grad)
+    cost = quad ? twin_tower_core<R, true, true>(sc, rows, my, lane, lo, hi, obs)
+                : twin_tower_core<R, true, false>(sc, rows, my, lane, lo, hi, obs);
+  else
+    cost = quad ? twin_tower_core<R, false, true>(sc, rows, my, lane, lo, hi, obs)
+                : twin_tower_core<R, false, false>(sc, rows, my, lane, lo, hi, obs);
+  cost = warp_sum_fixed(cost);
+  if (lane == 0) scr[2 * n + 96 * nv + part - 1] = cost;
+  __syncwarp();
+  twin_ext_arrive(twin_ext_count(ext));
+}
+
+// ext = number of helper warps (0: the aux warp does all the work; 1: + cube-obstacle
+// pairs; 2: + stability supports)
+template <typename R, bool WG, bool Q>
+__device__ R twin_tower_warp(const TowerScene<R>& sc, const R* rows, R* grad, R* scr, int lane, int ext = 0) {
+  const int n = sc.n_blocks;
+  const int nv = 4 * n;
+  R* gl = scr + 2 * n;
+  R cost = twin_tower_core<R, WG, Q>(sc, rows, gl + lane * nv, lane, ext >= 2 ? n - 1 : 0, 1 << 30, ext == 0);
   cost = warp_sum_fixed(cost);
   if (ext) {
-    twin_ext_sync();
-    cost += scr[2 * n + 64 * nv];
+    twin_ext_sync(twin_ext_count(ext));
+    cost += scr[2 * n + 96 * nv];
+    if (ext >= 2) cost += scr[2 * n + 96 * nv + 1];
   }
-  twin_reduce_slots<R, WG>(gl, nv, grad, lane, ext ? 64 : 32);
+  twin_reduce_slots<R, WG>(gl, nv, grad, lane, 32 * (1 + ext));
   __syncwarp();
   return cost;
 }
@@ -289,7 +307,7 @@ __device__ R twin_tower_warp(const TowerScene<R>& sc, const R* rows, R* grad, R*
 // written when want_grad.
 template <typename R, int KIND, int SPB, class TS>
 __device__ R twin_warp(const TS& ts, const R* rows, R* grad, R* scr, int lane, bool want_grad, bool quad,
-                      bool ext = false) {
+                      int ext = 0) {
   if constexpr (KIND == 1) {
     if (want_grad)
       return quad ? twin_tetris_warp<R, SPB, true, true>(ts, rows, grad, scr, lane)
