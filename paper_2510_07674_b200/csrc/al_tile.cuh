@@ -321,16 +321,16 @@ __device__ void al_eval(AlCtx<R>& C, const typename TwinSceneOf<R, KIND>::type& 
       if (C.prof.on && lane == 0) atomicAdd(&g_al_arrive[1][5], (unsigned long long)(clock64() - C.prof.t));
       R cpl = twin_warp<R, KIND, SPB>(tw, C.rows, C.gpose, C.scr, lane, want_grad, pquad, twin_ext);
       if (C.prof.on && lane == 0) atomicAdd(&g_al_arrive[1][6], (unsigned long long)(clock64() - C.prof.t));
-      if (lane == 0) {
-        if (sc.anchor) {
-          for (int bb = 0; bb < B; ++bb) {
-            const R wp = wrap_yaw(C.psi[bb]);
-            cpl += pquad ? wp * wp : fabs(wp);
-            if (want_grad) C.gpose[4 * bb + 3] += pquad ? R(2) * wp : (wp > R(0) ? R(1) : (wp < R(0) ? R(-1) : R(0)));
-          }
+      if (sc.anchor) {  // yaw anchor (trajopt.py:531-539): lane bb takes segment bb, warp-summed
+        R av = R(0);
+        for (int bb = lane; bb < B; bb += 32) {
+          const R wp = wrap_yaw(C.psi[bb]);
+          av += pquad ? wp * wp : fabs(wp);
+          if (want_grad) C.gpose[4 * bb + 3] += pquad ? R(2) * wp : (wp > R(0) ? R(1) : (wp < R(0) ? R(-1) : R(0)));
         }
-        C.scal[kCplace] = cpl;
+        cpl += warp_sum_fixed(av);
       }
+      if (lane == 0) C.scal[kCplace] = cpl;
     }
   } else if (w < C.L.NW / kTile) {
     // tower scenes: the last tile warps run parts of the twin first, handing them to the
