@@ -251,8 +251,8 @@ __device__ void al_eval(AlCtx<R>& C, const typename TwinSceneOf<R, KIND>::type& 
   const R w_start = R(prm.w_start);
   WpState<R> st;
   R obj_w = R(0), carm = R(0), cblk = R(0);
-  // tower twin helpers (twin_warp.cuh): the last tile warp takes the cube-obstacle pairs,
-  // the one before it the stability supports
+  // tower twin helpers (twin_warp.cuh): the last two tile warps take the stability
+  // supports and the cube-obstacle pairs
   const int twin_ext = KIND == 2 ? (C.L.NW >= 64 ? 2 : 1) : 0;
 
   // ---------------- P1: tile FK, sphere centres, placed poses ----------------------------
@@ -336,8 +336,11 @@ __device__ void al_eval(AlCtx<R>& C, const typename TwinSceneOf<R, KIND>::type& 
     // tower scenes: the last tile warps run parts of the twin first, handing them to the
     // aux warp at named barrier 1 (the twin bounds this phase)
     if constexpr (KIND == 2) {
-      const int part = C.L.NW / 32 - (tid >> 5);  // 1 = last tile warp, 2 = the one before
-      if (manip && part <= twin_ext) twin_tower_helper<R>(tw, C.rows, C.scr, lane, want_grad, pquad, part, twin_ext);
+      // 2 (stability) = last tile warp (the lightest: padding tiles), 1 (cube-obstacle
+      // pairs) = the one before it; with a single tile warp it takes part 1
+      const int back = C.L.NW / 32 - (tid >> 5);
+      const int part = twin_ext == 2 ? 3 - back : back;
+      if (manip && back <= twin_ext) twin_tower_helper<R>(tw, C.rows, C.scr, lane, want_grad, pquad, part, twin_ext);
     }
     // path length and start alignment moved here from P1: the tile warps have slack in P2
     // (the aux warp's placement twin bounds it), so P1 ends sooner
