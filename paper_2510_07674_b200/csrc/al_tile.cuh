@@ -913,6 +913,7 @@ __global__ void __launch_bounds__(kMaxAlThreads) k_solve_al(const TrajScene<R>* 
         const int w0 = bb * T;
         R qj = tlw.j < J ? C.x[w0 * kXS + tlw.j] : R(0);
         tile_polish<R>(tlw, ch, qj, sc.pick_pos[bb], sc.pick_yaw[bb]);
+        __syncwarp();  // the replica lanes' reads of x above precede lanes 0-7's writes
         if ((tid & 31) < kTile && tlw.j < J) C.x[w0 * kXS + tlw.j] = qj;
       }
     } else if (manip && (tid >> 3) < sc.B) {
