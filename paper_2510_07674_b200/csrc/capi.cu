@@ -6,6 +6,7 @@
 // ordering and the re-check, then reads back one small result block.
 #include <algorithm>
 #include <cstring>
+#include <map>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -17,6 +18,45 @@
 #include "launchers.hpp"
 
 namespace spasm {
+
+// Process-wide cache of the pinned result-staging buffers. Models are often short-lived (the
+// C4 replanning loop builds one per tick): cudaMallocHost / cudaFreeHost per model cost
+// milliseconds of driver time with a long tail, so released buffers are kept for reuse.
+// A buffer is released only after its model's last solve has read its results.
+namespace {
+std::mutex g_pin_mu;
+std::multimap<size_t, void*> g_pin_free;
+constexpr size_t kPinCacheMax = 32;
+
+cudaError_t pinned_get(void** p, size_t bytes, size_t* got) {
+  {
+    std::lock_guard<std::mutex> lk(g_pin_mu);
+    auto it = g_pin_free.lower_bound(bytes);
+    if (it != g_pin_free.end() && it->first <= 4 * bytes + 65536) {
+      *p = it->second;
+      *got = it->first;
+      g_pin_free.erase(it);
+      return cudaSuccess;
+    }
+  }
+  const cudaError_t e = cudaMallocHost(p, bytes);
+  *got = e == cudaSuccess ? bytes : 0;
+  return e;
+}
+
+void pinned_put(void* p, size_t bytes) {
+  if (!p) return;
+  {
+    std::lock_guard<std::mutex> lk(g_pin_mu);
+    if (g_pin_free.size() < kPinCacheMax) {
+      g_pin_free.emplace(bytes, p);
+      return;
+    }
+  }
+  cudaFreeHost(p);
+}
+}  // namespace
+
 
 static thread_local std::string g_last_error;
 void set_last_error(const std::string& msg) { g_last_error = msg; }
@@ -177,11 +217,10 @@ static int solve_impl(Model& m, const spasm_solve_config& cfg, const double* war
   int32_t* out_idx = reinterpret_cast<int32_t*>(out_recheck + cfg.p_return);
 
   if (m.pinned_bytes < L.res_bytes) {
-    if (m.pinned) cudaFreeHost(m.pinned);
+    pinned_put(m.pinned, m.pinned_bytes);
     m.pinned = nullptr;
     m.pinned_bytes = 0;
-    SPASM_CUDA_TRY(cudaMallocHost(&m.pinned, L.res_bytes));
-    m.pinned_bytes = L.res_bytes;
+    SPASM_CUDA_TRY(pinned_get(&m.pinned, L.res_bytes, &m.pinned_bytes));
   }
   char* host = static_cast<char*>(m.pinned);
 
@@ -632,7 +671,7 @@ int spasm_tower_model_create(spasm_model** out, int n_blocks, double side, doubl
 
 void spasm_model_destroy(spasm_model* model) {
   if (!model) return;
-  if (model->pinned) cudaFreeHost(model->pinned);
+  pinned_put(model->pinned, model->pinned_bytes);
   if (model->gexec) cudaGraphExecDestroy(model->gexec);
   if (model->cap) cudaStreamDestroy(model->cap);
   if (model->rp_dev) cudaFree(model->rp_dev);
