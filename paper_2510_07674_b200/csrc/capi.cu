@@ -27,6 +27,7 @@ namespace {
 std::mutex g_pin_mu;
 std::multimap<size_t, void*> g_pin_free;
 constexpr size_t kPinCacheMax = 32;
+}  // namespace
 
 cudaError_t pinned_get(void** p, size_t bytes, size_t* got) {
   {
@@ -55,7 +56,6 @@ void pinned_put(void* p, size_t bytes) {
   }
   cudaFreeHost(p);
 }
-}  // namespace
 
 
 static thread_local std::string g_last_error;

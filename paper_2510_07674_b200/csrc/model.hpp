@@ -5,6 +5,12 @@
 
 namespace spasm {
 
+// pinned staging buffers shared by all handles (capi.cu): get a buffer of >= bytes (the size
+// actually held is written to *got), put it back when the handle is done with it
+cudaError_t pinned_get(void** p, size_t bytes, size_t* got);
+void pinned_put(void* p, size_t bytes);
+
+
 enum class ModelKind { Tetris = 1, Tower = 2 };
 
 struct Model {

@@ -228,8 +228,7 @@ static int ensure_device(const Traj& tc) {
   if (e == cudaSuccess) e = cudaMemcpy(t.df, &t.hf, sizeof(TrajScene<float>), cudaMemcpyHostToDevice);
   if (e == cudaSuccess) e = cudaMemcpy(t.dd, &t.hd, sizeof(TrajScene<double>), cudaMemcpyHostToDevice);
   if (e == cudaSuccess && !t.pinned) {
-    t.pinned_bytes = 4096;
-    e = cudaHostAlloc(&t.pinned, t.pinned_bytes, cudaHostAllocDefault);
+    e = pinned_get(&t.pinned, 4096, &t.pinned_bytes);
   }
   if (e != cudaSuccess) {
     set_last_error(std::string("spasm_traj device upload: ") + cudaGetErrorString(e));
@@ -332,7 +331,7 @@ void spasm_traj_destroy(spasm_traj* t) {
   if (!t) return;
   if (t->df) cudaFree(t->df);
   if (t->dd) cudaFree(t->dd);
-  if (t->pinned) cudaFreeHost(t->pinned);
+  pinned_put(t->pinned, t->pinned_bytes);
   delete t;
 }
 
