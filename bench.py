@@ -397,28 +397,127 @@ def _oracle_solve(scene, over, stage1_only, seed, threads, max_restarts=None):
                           max_restarts=max_restarts)
 
 
+_REF = {}
+
+
+def _reference_impl():
+    """The reference's own CPU implementation when it is staged in baseline/_ref
+    (scripts/stage_reference.py: the offline pip install of /root/reference/pkg + the
+    variant-B fix), driven through its stock ``seqplace.bench.solve_scene``; otherwise the
+    float64 oracle port (oracle/pipeline.py)."""
+    if "kind" not in _REF:
+        path = os.path.join(ROOT, "baseline", "_ref")
+        _REF["kind"] = "port"
+        if os.path.isdir(os.path.join(path, "seqplace")) and os.environ.get("SPASM_REFERENCE_ARM", "ref") != "port":
+            sys.path.insert(0, path)
+            import seqplace.bench as rb
+
+            _REF.update(kind="reference", bench=rb, scenes={},
+                        orig={k: getattr(rb, k) for k in ("solve", "solve_al")})
+    return _REF["kind"]
+
+
+class _RefRun:
+    """One stock seqplace.bench.solve_scene call with the work it did recorded: the names the
+    reference's bench binds at import (bench.py:28-51) are wrapped so the stage-1 config /
+    report and the AL batch / outer count are seen on the way through (nothing is changed)."""
+
+    def __init__(self, success, time_ms, stage1_iterations, stage2_iterations):
+        self.success, self.time_ms = success, time_ms
+        self.stage1_iterations, self.stage2_iterations = stage1_iterations, stage2_iterations
+
+
+def _reference_solve(scene_name, over, stage1_only, seed, threads, max_restarts=None):
+    rb, rec = _REF["bench"], {}
+    if scene_name not in _REF["scenes"]:
+        from oracle.refscene import ref_scene
+
+        _REF["scenes"][scene_name] = ref_scene(scene_name)
+    scene = _REF["scenes"][scene_name]
+
+    def w_solve(model, config, **kw):
+        res = _REF["orig"]["solve"](model, config, **kw)
+        rec["cfg"], rec["res"] = config, res
+        return res
+
+    def w_al(values, *a, **kw):
+        rec["P"] = len(values)
+        try:
+            al = _REF["orig"]["solve_al"](values, *a, **kw)
+        except rb.TrajOptFailure as exc:
+            rec["outers"], rec["inner"] = len(exc.report.outers), a[2].inner_steps
+            raise
+        rec["outers"], rec["inner"] = len(al.report.outers), a[2].inner_steps
+        return al
+
+    rb.solve, rb.solve_al = w_solve, w_al
+    try:
+        so = dict(over)
+        if max_restarts:
+            so["max_restarts"] = max_restarts
+        sol = rb.solve_scene(scene, seed=seed, threads=threads, solver_overrides=so, no_trajopt=stage1_only)
+    finally:
+        rb.solve, rb.solve_al = _REF["orig"]["solve"], _REF["orig"]["solve_al"]
+    cfg, res = rec["cfg"], rec["res"]
+    runs = res.report.restarts + 1 if res.success else cfg.max_restarts
+    it2 = rec.get("outers", 0) * rec.get("P", 0) * rec.get("inner", 0)
+    return _RefRun(bool(sol.success), sol.time_ms, runs * cfg.m * (cfg.k_lin + cfg.k_quad), it2)
+
+
+def _cpu_solve(scene, scene_name, over, stage1_only, seed, threads, max_restarts=None):
+    if _reference_impl() == "reference":
+        return _reference_solve(scene_name, over, stage1_only, seed, threads, max_restarts)
+    return _oracle_solve(scene, over, stage1_only, seed, threads, max_restarts)
+
+
+def _host_info():
+    model = ""
+    try:
+        with open("/proc/cpuinfo") as f:
+            model = next((ln.split(":", 1)[1].strip() for ln in f if ln.startswith("model name")), "")
+    except OSError:
+        pass
+    return {"cpu_model": model, "nproc": os.cpu_count(), "numpy": np.__version__}
+
+
+def _arm_label(threads):
+    if _reference_impl() == "reference":
+        return (f"stock seqplace.bench.solve_scene from baseline/_ref (reference pkg, variant-B fix), numpy "
+                f"float64, threads={threads}")
+    return f"oracle/pipeline.py (float64 numpy port of the reference), threads={threads}"
+
+
 def cpu_baseline(args, budget_s=20.0):
-    """The CPU oracle port (oracle/pipeline.py, float64 numpy) timed on this host's cores
-    on a bounded sample of the same workload."""
+    """The reference's CPU implementation (baseline/_ref when staged, else the oracle port)
+    timed on this host's cores on a bounded sample of the same workload, with all host
+    threads and with threads=1."""
     from paper_2510_07674_b200.problems import load_scene
 
     scene_name, over, stage1_only, desc = WORKLOADS[args.workload]
     scene = load_scene(scene_name)
     threads = os.cpu_count() or 1
-    its, t_total, solves, times = 0, 0.0, 0, []
-    t_start = time.perf_counter()
     # large stage-1-only workloads: one restart per sample solve; pipelines: whole solves
     mr = 1 if stage1_only else None
-    while time.perf_counter() - t_start < budget_s and solves < 3:
-        r = _oracle_solve(scene, over, stage1_only, solves, threads, max_restarts=mr)
-        t_total += r.time_ms * 1e-3
-        times.append(r.time_ms)
-        its += r.stage1_iterations + r.stage2_iterations
-        solves += 1
-    return {"value": its / t_total, "unit": "particle-iterations/s", "cores": threads, "kind": "port",
-            "p50_solve_ms": statistics.median(times),
-            "sample": f"{solves} {'single-restart stage-1' if stage1_only else 'full two-stage'} solve(s) of "
-                      f"{scene_name} (oracle/pipeline.py, numpy float64, {threads} threads)"}
+
+    def sample(th, budget, max_solves):
+        its, t_total, times = 0, 0.0, []
+        t_start = time.perf_counter()
+        while time.perf_counter() - t_start < budget and len(times) < max_solves:
+            r = _cpu_solve(scene, scene_name, over, stage1_only, len(times), th, max_restarts=mr)
+            t_total += r.time_ms * 1e-3
+            times.append(r.time_ms)
+            its += r.stage1_iterations + r.stage2_iterations
+        return its / t_total, times
+
+    value, times = sample(threads, budget_s, 3)
+    one = None
+    if threads > 1 and statistics.median(times) < 8000:  # threads=1 figure, one bounded solve
+        v1, t1 = sample(1, 0.0, 1)
+        one = {"value": v1, "p50_solve_ms": statistics.median(t1), "cores": 1}
+    return {"value": value, "unit": "particle-iterations/s", "cores": threads, "kind": _reference_impl(),
+            "p50_solve_ms": statistics.median(times), "threads_1": one, "host": _host_info(),
+            "sample": f"{len(times)} {'single-restart stage-1' if stage1_only else 'full two-stage'} solve(s) of "
+                      f"{scene_name} ({_arm_label(threads)})"}
 
 
 def run_reference(args):
@@ -431,24 +530,30 @@ def run_reference(args):
     scene = load_scene(scene_name)
     threads = os.cpu_count() or 1
     mr = 1 if stage1_only else None
+    kind = _reference_impl()
     for i in range(args.warmup):  # warm numpy / thread pools on cheap stage-1 samples
-        _oracle_solve(scene, over, True, 100000 + i, threads, max_restarts=1)
+        _cpu_solve(scene, scene_name, over, True, 100000 + i, threads, max_restarts=1)
     times, its, succ = [], 0, 0
     for i in range(args.steps):
-        r = _oracle_solve(scene, over, stage1_only, i, threads, max_restarts=mr)
+        r = _cpu_solve(scene, scene_name, over, stage1_only, i, threads, max_restarts=mr)
         times.append(r.time_ms)
         its += r.stage1_iterations + r.stage2_iterations
         succ += int(r.success)
     value = its / (sum(times) * 1e-3)
+    from paper_2510_07674_b200.bench_api import _solver_config, effective_max_restarts
+
+    c = _solver_config(scene, 0, over, False)
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "particle-iterations/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": sum(times) / args.steps,
         "p50_solve_ms": statistics.median(times), "success_rate": succ / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": desc, "scene": scene_name, **over, "stage2": not stage1_only,
-                   "max_restarts": mr if mr else "STEP_CAP"},
-        "cpu_baseline": {"value": value, "unit": "particle-iterations/s", "cores": threads, "kind": "port",
-                         "sample": f"{args.steps} solves of {scene_name} (oracle/pipeline.py, numpy float64)"},
+        "config": {"workload": desc, "scene": scene_name, "n": c.n, "m": c.m, "k_lin": c.k_lin, "k_quad": c.k_quad,
+                   "max_restarts": effective_max_restarts(c), "p_return": c.p_return, "stage2": not stage1_only},
+        "cpu_baseline": {"value": value, "unit": "particle-iterations/s", "cores": threads, "kind": kind,
+                         "host": _host_info(),
+                         "sample": f"{args.steps} {'stage-1 (bounded to 1 restart)' if stage1_only else 'full two-stage'} "
+                                   f"solves of {scene_name} ({_arm_label(threads)})"},
         "e2e": {"value": value, "unit": "particle-iterations/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line))

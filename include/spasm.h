@@ -49,6 +49,10 @@ typedef struct spasm_model spasm_model; /* opaque placement cost model (scene ta
 
 const char* spasm_last_error(void);
 int spasm_version(void);
+/* sizeof() of an ABI struct by its type name ("spasm_solve_config", "spasm_solve_report",
+ * "spasm_chain", "spasm_traj_desc", "spasm_al_config", "spasm_al_result"); -1 if unknown.
+ * Lets a foreign binder (ctypes / cffi) check its struct mirrors against the library. */
+int64_t spasm_abi_sizeof(const char* type_name);
 /* Process-wide tuning switches (not in the reference; results stay within the parity
  * tolerances under every setting). "stage1_tile": -1 auto (default: on), 0 = generic
  * stage-1 kernels only, 1..4 = on (the fp32 tetris tile kernels, 4 lanes per particle;

@@ -10,6 +10,7 @@ from __future__ import annotations
 import math
 import time
 from dataclasses import dataclass
+from typing import Optional
 
 import numpy as np
 
@@ -25,6 +26,14 @@ class OracleSceneResult:
     stage1_iterations: int
     stage2_iterations: int
     max_violation: float
+    # bookkeeping the pipeline-parity tests compare (bench.py:168-268 intermediates)
+    restarts: int = -1
+    stage1_indices: Optional[np.ndarray] = None
+    kept: Optional[np.ndarray] = None
+    accepted_outer: int = -1
+    al_particle: int = -1
+    objective: float = math.nan
+    lift_failed: bool = False
 
 
 def effective_max_restarts(cfg):  # bench.py:80-85
@@ -32,7 +41,8 @@ def effective_max_restarts(cfg):  # bench.py:80-85
     return cfg.max_restarts if per == 0 else min(cfg.max_restarts, max(1, STEP_CAP // per))
 
 
-def solve_scene(scene, seed=0, threads=1, solver_overrides=None, no_trajopt=False, max_restarts=None):
+def solve_scene(scene, seed=0, threads=1, solver_overrides=None, no_trajopt=False, max_restarts=None,
+                place_mode=None):
     o = stage1.oracle_model(scene.problem)
     cfg = stage1.OracleConfig(**{**scene.solver_overrides, **(solver_overrides or {})})
     cfg.seed = seed
@@ -40,23 +50,28 @@ def solve_scene(scene, seed=0, threads=1, solver_overrides=None, no_trajopt=Fals
     t0 = time.perf_counter()
     res = stage1.solve(o, cfg, threads=threads)
     it1 = (res.restarts + 1 if res.success else cfg.max_restarts) * cfg.m * (cfg.k_lin + cfg.k_quad)
+    rec = dict(restarts=int(res.restarts), stage1_indices=np.asarray(res.indices))
     if not res.success or scene.chain is None or no_trajopt:
-        return OracleSceneResult(bool(res.success), (time.perf_counter() - t0) * 1e3, it1, 0, math.nan)
+        return OracleSceneResult(bool(res.success), (time.perf_counter() - t0) * 1e3, it1, 0, math.nan, **rec)
     tcfg = stage2.TrajConfig(**scene.trajopt_overrides)
+    kept = None
     try:
         ends, kept = stage2.lift_placements(scene.problem, res.particles, scene.chain, scene.grasp, seed=seed,
                                             static_centers=scene.obstacle_centers,
                                             static_radii=scene.obstacle_radii)
         vals = stage2.init_trajectories(ends, scene.chain, tcfg, stage2.trajectory_stream(seed))
         al = stage2.solve_al(vals, scene.problem, scene.chain, tcfg, scene.grasp, scene.obstacle_centers,
-                             scene.obstacle_radii)
+                             scene.obstacle_radii, place_mode=place_mode)
     except stage2.LiftFailure:
-        return OracleSceneResult(False, (time.perf_counter() - t0) * 1e3, it1, 0, math.nan)
+        return OracleSceneResult(False, (time.perf_counter() - t0) * 1e3, it1, 0, math.nan, lift_failed=True, **rec)
     except stage2.TrajOptFailure as exc:
         it2 = len(exc.report) * len(vals) * tcfg.inner_steps
-        return OracleSceneResult(False, (time.perf_counter() - t0) * 1e3, it1, it2, exc.best_violation)
+        return OracleSceneResult(False, (time.perf_counter() - t0) * 1e3, it1, it2, exc.best_violation,
+                                 kept=np.asarray(kept), accepted_outer=-1, **rec)
     time_ms = (time.perf_counter() - t0) * 1e3
     it2 = len(al.outers) * len(vals) * tcfg.inner_steps
     g = stage2.build_geometry(scene.problem, scene.chain, scene.grasp, scene.obstacle_centers, scene.obstacle_radii)
     ok, worst = stage2.validate(al.values, g, tcfg.validation_epsilon)
-    return OracleSceneResult(bool(ok), time_ms, it1, it2, float(worst))
+    return OracleSceneResult(bool(ok), time_ms, it1, it2, float(worst), kept=np.asarray(kept),
+                             accepted_outer=len(al.outers) - 1, al_particle=int(al.particle_index),
+                             objective=float(al.objective), **rec)

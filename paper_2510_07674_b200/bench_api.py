@@ -53,6 +53,10 @@ class SceneSolution:
     # every satisfying stage-1 particle returned (the replanning loop warm-starts from them)
     stats: dict = field(default_factory=dict)
     particles: Optional[np.ndarray] = None
+    # the pipeline's intermediate decisions (stage-1 restart + returned batch indices, lift
+    # kept set, accepted AL outer / particle / objective), read after the timed span; the
+    # pipeline-parity tests compare them with oracle/pipeline.py
+    bookkeeping: dict = field(default_factory=dict)
 
 
 def solve_scene(scene: Scene, *, seed: int = 0, threads: int = 1, solver_overrides: Optional[dict] = None,
@@ -86,15 +90,19 @@ def solve_scene(scene: Scene, *, seed: int = 0, threads: int = 1, solver_overrid
              "stage1_ms": (time.perf_counter() - t0) * 1e3}
     if not result.success:
         return SceneSolution(False, (time.perf_counter() - t0) * 1e3, result.report.restarts, result.report.steps,
-                             math.nan, stats=stats)
+                             math.nan, stats=stats, bookkeeping={"restarts": int(result.report.restarts)})
     if not run_stage2:
         time_ms = (time.perf_counter() - t0) * 1e3
         best = result.particles[0]
         ok = bool(np.asarray(model.satisfaction(best[None, :], config.epsilon))[0])
         return SceneSolution(ok, time_ms, result.report.restarts, result.report.steps, float(result.costs[0]),
-                             placement=best.copy(), stats=stats, particles=result.particles.copy())
+                             placement=best.copy(), stats=stats, particles=result.particles.copy(),
+                             bookkeeping={"restarts": int(result.report.restarts),
+                                          "stage1_indices": np.asarray(result.indices).copy()})
     from .trajopt import solve_stage2
 
     sol = solve_stage2(scene, result, config, seed, trajopt_overrides, t0, precision=precision)
     sol.stats = {**stats, **sol.stats}
+    sol.bookkeeping = {"restarts": int(result.report.restarts), "stage1_indices": np.asarray(result.indices).copy(),
+                       **sol.bookkeeping}
     return sol

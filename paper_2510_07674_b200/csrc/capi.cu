@@ -397,6 +397,18 @@ extern "C" {
 const char* spasm_last_error(void) { return spasm::last_error(); }
 int spasm_version(void) { return 1; }
 
+int64_t spasm_abi_sizeof(const char* type_name) {
+  if (type_name == nullptr) return -1;
+  const std::string n(type_name);
+  if (n == "spasm_solve_config") return sizeof(spasm_solve_config);
+  if (n == "spasm_solve_report") return sizeof(spasm_solve_report);
+  if (n == "spasm_chain") return sizeof(spasm_chain);
+  if (n == "spasm_traj_desc") return sizeof(spasm_traj_desc);
+  if (n == "spasm_al_config") return sizeof(spasm_al_config);
+  if (n == "spasm_al_result") return sizeof(spasm_al_result);
+  return -1;
+}
+
 static int fill_bounds(Model& m, int D, const double* lower, const double* upper) {
   SPASM_REQUIRE(D >= 1 && D <= kMaxDim, "state dimension out of range (1..128)");
   for (int d = 0; d < D; ++d) {

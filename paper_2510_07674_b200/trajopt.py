@@ -774,19 +774,23 @@ def solve_stage2(scene, result, config, seed, trajopt_overrides, t0, precision: 
              "stage2_launches": 6, "al_device_ms": float(res.device_ms), "lift_targets": len(pl) * geo.n_segments
              + geo.n_segments}
     if status == nat.SPASM_LIFT_FAILURE:
-        return SceneSolution(False, time_ms, result.report.restarts, result.report.steps, math.nan, stats=stats)
+        return SceneSolution(False, time_ms, result.report.restarts, result.report.steps, math.nan, stats=stats,
+                             bookkeeping={"lift_failed": True})
+    kept = lift.kept[:int(res.n_particles)].cpu().numpy()
+    book = {"kept": kept, "accepted_outer": int(res.accepted_outer), "al_particle": int(res.particle_index),
+            "objective": float(res.objective), "lift_failed": False}
     if status == nat.SPASM_AL_FAILURE:
         w = float(res.least_violation)
         return SceneSolution(False, time_ms, result.report.restarts, result.report.steps, w, max_violation=w,
-                             stats=stats)
+                             stats=stats, bookkeeping=book)
     traj = _particle_trajectory(best.double().cpu().numpy(), geo)
     feasible, worst = validate(traj, scene.problem, scene.chain, grasp=scene.grasp,
                                static_centers=scene.obstacle_centers, static_radii=scene.obstacle_radii,
                                epsilon=tcfg.validation_epsilon, precision="fp64")
-    kept = lift.kept[:int(res.n_particles)].cpu().numpy()
     return SceneSolution(bool(feasible), time_ms, result.report.restarts, result.report.steps, worst,
                          placement=np.asarray(result.particles)[int(kept[res.particle_index])].copy(),
-                         trajectory=traj, path_length=trajectory_path_length(traj), max_violation=worst, stats=stats)
+                         trajectory=traj, path_length=trajectory_path_length(traj), max_violation=worst, stats=stats,
+                         bookkeeping=book)
 
 
 def solve_motion_scene(scene, seed, trajopt_overrides, precision: str = "fp32"):

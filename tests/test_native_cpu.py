@@ -113,3 +113,31 @@ def test_trajopt_config_validation_mirrors_reference():
                 {"outer_iters": 0}, {"inner_steps": 0}, {"lr_init": 0.0}, {"validation_epsilon": 0.0}):
         with pytest.raises(ValueError):
             TrajOptConfig(**bad)
+
+
+ABI_STRUCTS = ["spasm_solve_config", "spasm_solve_report", "spasm_chain", "spasm_traj_desc", "spasm_al_config",
+               "spasm_al_result"]
+
+
+@pytest.mark.parametrize("name", ABI_STRUCTS)
+def test_abi_struct_sizes_match_ctypes_mirrors(name):
+    lib = nat.load()
+    assert lib.spasm_abi_sizeof(name.encode()) == ctypes.sizeof(getattr(nat, name))
+
+
+def test_abi_sizeof_unknown_type():
+    assert nat.load().spasm_abi_sizeof(b"no_such_struct") == -1
+
+
+def test_integration_doc_ctypes_stub_matches_library():
+    """Execute INTEGRATION.md's reference-side ctypes stub against the built library: every
+    argtypes line binds an exported symbol and the documented SolveConfig has the library's
+    size (a short mirror would make spasm_solve read past the caller's struct)."""
+    doc = open(os.path.join(ROOT, "INTEGRATION.md")).read()
+    blocks = re.findall(r"```python\n(.*?)```", doc, re.S)
+    stub = next(b for b in blocks if "class SolveConfig" in b)
+    stub = stub.replace('ctypes.CDLL("paper_2510_07674_b200/libspasm.so")', "ctypes.CDLL(LIBPATH)")
+    ns = {"LIBPATH": nat.load()._name}
+    exec(compile(stub, "INTEGRATION.md", "exec"), ns)
+    assert ctypes.sizeof(ns["SolveConfig"]) == ctypes.sizeof(nat.spasm_solve_config)
+    assert [f[0] for f in ns["SolveConfig"]._fields_] == [f[0] for f in nat.spasm_solve_config._fields_]

@@ -23,7 +23,7 @@ from paper_2510_07674_b200.problems import as_cost_model, load_scene
 
 pytestmark = pytest.mark.gpu
 
-SCENES = ["tetris5", "tetris8", "single1", "tower4", "tower3c", "tower6r"]
+SCENES = ["tetris4", "tetris5", "tetris6", "tetris8", "single1", "tower4", "tower3c", "tower6r"]
 VARIANTS = [4]
 
 
@@ -118,14 +118,14 @@ def test_tile_full_schedule_tracks_generic_kernel(variant):
     assert abs(int(sat0.sum()) - int(sat1.sum())) <= max(2, 0.1 * sat0.sum())
 
 
-@pytest.mark.parametrize("name", ["tetris5", "tetris8"])
+@pytest.mark.parametrize("name", ["tetris4", "tetris5", "tetris6", "tetris8"])
 def test_tile_solve_outcome_matches_generic(name):
     scene = load_scene(name)
     m = as_cost_model(scene.problem, precision="fp32")
     o = orc.oracle_model(scene.problem)
     over = {"n": 8192, "m": 1024} if name == "tetris8" else {}
     wins = [0, 0]
-    for seed in range(4):
+    for seed in range(8):
         cfg = po.OptimizerConfig(**{**scene.solver_overrides, **over, "seed": seed, "max_restarts": 3})
         for k, mode in enumerate((0, -1)):
             _set_tile(mode)
@@ -133,7 +133,8 @@ def test_tile_solve_outcome_matches_generic(name):
             wins[k] += int(res.success)
             if res.success:
                 assert np.all(o.evaluate(res.particles, "quadratic") < cfg.epsilon * 1.01)
-    assert abs(wins[0] - wins[1]) <= 1
+    print(name, "successes generic / tile over 8 seeds:", wins)
+    assert wins[0] == wins[1]
 
 
 def _key_to_cost(keys):

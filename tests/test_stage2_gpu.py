@@ -8,7 +8,8 @@ Tolerances:
       whole AL solves: identical accepted outer, particle index and feasibility flags,
       objective rtol 1e-6 (hundreds of chained descent steps, as the oracle's own pin).
   fp32 (throughput path): costs and constraints rtol 1e-4 (atol 1e-5) vs the fp64 oracle on
-      the same fp32-rounded inputs; gradients within 1e-3 of the gradient scale.
+      the same fp32-rounded inputs; gradients per particle within relative norm error 1e-4
+      (north_star's rtol 1e-4, measured as the reference's AL-gradient tests measure it).
 """
 from __future__ import annotations
 
@@ -16,7 +17,7 @@ import numpy as np
 import pytest
 import torch
 
-from conftest import golden
+from conftest import golden, rel_err
 from oracle import stage2 as o2
 from paper_2510_07674_b200 import trajopt as tj
 from paper_2510_07674_b200.problems import load_scene
@@ -114,7 +115,12 @@ def test_al_value_and_gradient_vs_oracle_near_feasible(scene_name):
         lag32, grad32 = tj.al_value_and_gradient(v32, sc.problem, sc.chain, cfg, lam, mu, mode=mode, precision="fp32",
                                                  **kw)
         np.testing.assert_allclose(lag32, rl, rtol=1e-4, atol=1e-4)
-        assert np.abs(grad32 - rg).max() <= 1e-3 * max(np.abs(rg).max(), 1.0)
+        # north_star: per-particle gradients within rtol 1e-4 (fp32), as the per-particle
+        # relative norm error the reference's own AL-gradient tests use (conftest.rel_err)
+        per = [rel_err(grad32[p], rg[p]) for p in range(len(rg))]
+        print(scene_name, mode, "fp32 AL gradient per-particle rel err max", max(per),
+              "elementwise max / scale", np.abs(grad32 - rg).max() / max(np.abs(rg).max(), 1.0))
+        assert max(per) <= 1e-4, per
 
 
 @pytest.mark.parametrize("scene_name", ["tower4", "tetris5", "corridor3"])
