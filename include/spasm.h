@@ -53,6 +53,9 @@ int spasm_version(void);
  * "spasm_chain", "spasm_traj_desc", "spasm_al_config", "spasm_al_result"); -1 if unknown.
  * Lets a foreign binder (ctypes / cffi) check its struct mirrors against the library. */
 int64_t spasm_abi_sizeof(const char* type_name);
+/* Release the process-wide cache of pinned result-staging buffers (kept across model /
+ * trajectory handles, capped at 32 buffers and 64 MB). Always SPASM_OK. */
+int spasm_trim(void);
 /* Process-wide tuning switches (not in the reference; results stay within the parity
  * tolerances under every setting). "stage1_tile": -1 auto (default: on), 0 = generic
  * stage-1 kernels only, 1..4 = on (the fp32 tetris tile kernels, 4 lanes per particle;

@@ -26,7 +26,9 @@ namespace spasm {
 namespace {
 std::mutex g_pin_mu;
 std::multimap<size_t, void*> g_pin_free;
-constexpr size_t kPinCacheMax = 32;
+size_t g_pin_bytes = 0;                        // bytes held by the free list
+constexpr size_t kPinCacheMax = 32;            // entries
+constexpr size_t kPinCacheBytes = 64u << 20;   // and bytes (spasm_trim releases everything)
 }  // namespace
 
 cudaError_t pinned_get(void** p, size_t bytes, size_t* got) {
@@ -36,6 +38,7 @@ cudaError_t pinned_get(void** p, size_t bytes, size_t* got) {
     if (it != g_pin_free.end() && it->first <= 4 * bytes + 65536) {
       *p = it->second;
       *got = it->first;
+      g_pin_bytes -= it->first;
       g_pin_free.erase(it);
       return cudaSuccess;
     }
@@ -49,14 +52,25 @@ void pinned_put(void* p, size_t bytes) {
   if (!p) return;
   {
     std::lock_guard<std::mutex> lk(g_pin_mu);
-    if (g_pin_free.size() < kPinCacheMax) {
+    if (g_pin_free.size() < kPinCacheMax && g_pin_bytes + bytes <= kPinCacheBytes) {
       g_pin_free.emplace(bytes, p);
+      g_pin_bytes += bytes;
       return;
     }
   }
   cudaFreeHost(p);
 }
 
+// release every cached pinned buffer (spasm_trim)
+void pinned_trim() {
+  std::multimap<size_t, void*> drop;
+  {
+    std::lock_guard<std::mutex> lk(g_pin_mu);
+    drop.swap(g_pin_free);
+    g_pin_bytes = 0;
+  }
+  for (auto& kv : drop) cudaFreeHost(kv.second);
+}
 
 static thread_local std::string g_last_error;
 void set_last_error(const std::string& msg) { g_last_error = msg; }
@@ -152,7 +166,7 @@ static SolveLayout make_layout(int D, const spasm_solve_config& cfg, int64_t n_w
   return L;
 }
 
-static int validate_cfg(const spasm_solve_config* cfg) {
+int validate_cfg(const spasm_solve_config* cfg) {
   SPASM_REQUIRE(cfg != nullptr, "null solve config");
   SPASM_REQUIRE(cfg->m >= 1 && cfg->m <= cfg->n, "need 1 <= m <= n");
   SPASM_REQUIRE(cfg->n <= (int64_t)0xFFFFFFFF, "n exceeds 2^32 rows");
@@ -227,9 +241,17 @@ static int solve_impl(Model& m, const spasm_solve_config& cfg, const double* war
   if (n_warm > 0)
     SPASM_CUDA_TRY(cudaMemcpyAsync(warm_dev, warm_host, (size_t)n_warm * D * 8, cudaMemcpyHostToDevice, s));
 
-  cudaEvent_t e0, e1;
-  SPASM_CUDA_TRY(cudaEventCreate(&e0));
-  SPASM_CUDA_TRY(cudaEventCreate(&e1));
+  // the timing events are destroyed on every return path (early errors included)
+  struct EventPair {
+    cudaEvent_t a = nullptr, b = nullptr;
+    ~EventPair() {
+      if (a) cudaEventDestroy(a);
+      if (b) cudaEventDestroy(b);
+    }
+  } ev;
+  SPASM_CUDA_TRY(cudaEventCreate(&ev.a));
+  SPASM_CUDA_TRY(cudaEventCreate(&ev.b));
+  cudaEvent_t e0 = ev.a, e1 = ev.b;
   SPASM_CUDA_TRY(cudaEventRecord(e0, s));
 
   int total_steps = 0, total_flagged = 0, launches = 0;
@@ -381,8 +403,6 @@ static int solve_impl(Model& m, const spasm_solve_config& cfg, const double* war
   float ms = 0.f;
   cudaEventElapsedTime(&ms, e0, e1);
   rep->device_ms = ms;
-  cudaEventDestroy(e0);
-  cudaEventDestroy(e1);
   return rc;
 }
 
@@ -396,6 +416,11 @@ extern "C" {
 
 const char* spasm_last_error(void) { return spasm::last_error(); }
 int spasm_version(void) { return 1; }
+
+int spasm_trim(void) {
+  spasm::pinned_trim();
+  return SPASM_OK;
+}
 
 int64_t spasm_abi_sizeof(const char* type_name) {
   if (type_name == nullptr) return -1;

@@ -9,6 +9,7 @@ namespace spasm {
 // actually held is written to *got), put it back when the handle is done with it
 cudaError_t pinned_get(void** p, size_t bytes, size_t* got);
 void pinned_put(void* p, size_t bytes);
+void pinned_trim();
 
 
 enum class ModelKind { Tetris = 1, Tower = 2 };

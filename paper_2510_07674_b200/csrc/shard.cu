@@ -228,15 +228,15 @@ static int shard_descend_impl(const Model& m, const spasm_solve_config& cfg, int
   return SPASM_OK;
 }
 
+int validate_cfg(const spasm_solve_config* cfg);  // capi.cu: the single-GPU solve's checks
+
+// the single-GPU validator plus the shard path's own row bound (row 0xFFFFFFFF is the
+// padding sentinel of the elite runs)
 static int validate_shard_cfg(const spasm_model* model, const spasm_solve_config* cfg) {
   SPASM_REQUIRE(model != nullptr, "null model");
-  SPASM_REQUIRE(cfg != nullptr, "null solve config");
-  SPASM_REQUIRE(cfg->m >= 1 && cfg->m <= cfg->n, "need 1 <= m <= n");
+  const int r = validate_cfg(cfg);
+  if (r) return r;
   SPASM_REQUIRE(cfg->n < (int64_t)0xFFFFFFFF, "n exceeds 2^32 - 1 rows");
-  SPASM_REQUIRE(cfg->k_lin >= 0 && cfg->k_quad >= 0, "step counts must be nonnegative");
-  SPASM_REQUIRE(cfg->eta_init > 0 && cfg->alpha > 0, "learning rates must be positive");
-  SPASM_REQUIRE(cfg->epsilon > 0, "epsilon must be positive");
-  SPASM_REQUIRE(cfg->p_return >= 1, "p_return must be >= 1");
   return SPASM_OK;
 }
 

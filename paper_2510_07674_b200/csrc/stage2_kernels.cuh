@@ -123,7 +123,7 @@ __global__ void __launch_bounds__(MAXT) k_ik_group(const TrajScene<R>* __restric
       g.init(seedseq_pcg64_dev(seed + (uint64_t)a * draw_stride, (uint64_t)t));
       g.advance((uint64_t)tile * J + tl.j);
       const double lo = ch.lo64[tl.j], hi = ch.hi64[tl.j];
-      qj = (R)(lo + (hi - lo) * g.next_double());
+      qj = (R)__dadd_rn(lo, __dmul_rn(__dsub_rn(hi, lo), g.next_double()));  // no FMA: numpy's rounding
     }
     R score;
     const bool ok = tile_ik<R>(tl, ch, qj, tp, ty, max_iters, R(damping), &score);
@@ -291,7 +291,7 @@ __global__ void k_init_traj(const TrajScene<R>* __restrict__ g_scene, const R* _
     g.init(st);
     g.advance((uint64_t)(((p * B + b) * K + (k - 1)) * J + j));
     const double lo = ch.lo64[j], hi = ch.hi64[j];
-    return lo + (hi - lo) * g.next_double();
+    return __dadd_rn(lo, __dmul_rn(__dsub_rn(hi, lo), g.next_double()));  // no FMA: numpy's rounding
   };
   double v;
   if (t == T - 1) {

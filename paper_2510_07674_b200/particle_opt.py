@@ -520,19 +520,26 @@ def solve(cost_model: CostModel, config: OptimizerConfig, *, warm_seeds=None, th
 
 
 class _Workspace:
-    """Device workspace cache keyed by (model handle, dtype, n, m, p_return, n_warm)."""
+    """Device scratch for ``spasm_solve``, keyed by what sizes it (dtype, D, n, m, p_return,
+    n_warm, device) -- not by the model: the buffer is plain scratch, so the C4 replanning
+    loop's per-tick models share one entry instead of leaving one per dead model behind.
+    At most ``cap`` entries are kept (least recently used dropped). A model's cached CUDA
+    graph records the workspace pointer and is re-captured if it changes (capi.cu)."""
 
-    def __init__(self):
+    def __init__(self, cap: int = 8):
         self._cache = {}
+        self._cap = cap
 
     def get(self, model: NativeCostModel, cfg, n_warm: int):
         torch = _torch()
-        key = (id(model), model.dtype_id, cfg.n, cfg.m, cfg.p_return, n_warm, torch.cuda.current_device())
+        key = (model.dtype_id, model.dimension, cfg.n, cfg.m, cfg.p_return, n_warm, torch.cuda.current_device())
         nbytes = nat.load().spasm_solve_workspace_bytes(model.handle, model.dtype_id, ctypes_byref(cfg), n_warm)
-        buf = self._cache.get(key)
+        buf = self._cache.pop(key, None)
         if buf is None or buf.numel() < nbytes:
             buf = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
-            self._cache[key] = buf
+        self._cache[key] = buf  # most recently used last
+        while len(self._cache) > self._cap:
+            self._cache.pop(next(iter(self._cache)))
         return buf
 
 
