@@ -38,8 +38,14 @@ WORKLOADS = {
     "c1": ("single1", {}, False,
            "C1 7-DOF arm, single-block pick-and-place, 1024 particles, stage 1 + stage 2 (32 waypoints)"),
     "c2": ("tower3c", {}, False,
-           "C2 3-block stacking with cuboid obstacles (sphere-grid cuboids), 16k particles, stage 1 + stage 2"),
+           "C2 3-block stacking with cuboid obstacles, 16k particles, stage 1 + stage 2; cuboids 0.2x0.2x0.3 m and "
+           "0.1x0.1x0.2 m as grids of r=0.05 m spheres at 0.1 m pitch (2x2x3 + 1x1x2 = 14 obstacle spheres)"),
     "c3": ("tetris5", {"n": 65536, "m": 8192}, True, "C3 Tetris packing, 5 objects, 64k particles, stage 1"),
+    "c3p": ("tetris5", {"n": 65536, "m": 8192}, False,
+            "C3 Tetris packing, 5 objects, 64k particles, stage 1 + stage 2 (motion-constrained placements: lift + "
+            "trajectory AL, B=5, T=11)"),
+    "c3_4": ("tetris4", {"n": 65536, "m": 8192}, True, "C3 Tetris packing, 4 objects, 64k particles, stage 1"),
+    "c3_6": ("tetris6", {"n": 65536, "m": 8192}, True, "C3 Tetris packing, 6 objects, 64k particles, stage 1"),
     "c4": ("tower6r", {"n": 16384, "m": 2048}, True,
            "C4 reactive replanning: 6-block rearrangement, one sphere obstacle moving 3 cm per tick, each tick "
            "warm-started from the previous placement, 16k particles, stage 1"),
@@ -50,8 +56,11 @@ WORKLOADS = {
 # ---------------------------------------------------------------------------
 # algorithmic work counts
 # ---------------------------------------------------------------------------
-def stage1_flops_per_iteration(model, mode="linear"):
-    """FP32 FLOPs of one fused cost-gradient-update step of one particle."""
+def stage1_flops_per_iteration(model, mode="linear", gradient_only=False):
+    """FP32 FLOPs of one fused cost-gradient-update step of one particle.
+    ``gradient_only``: the reference's step evaluates the gradient only (particle_opt.py:
+    214-228), so its count drops the per-pair cost accumulation (2 flops per pair linear,
+    3 quadratic) and the height-term cost."""
     from paper_2510_07674_b200.problems import TetrisCostModel
 
     p = model.problem
@@ -62,12 +71,18 @@ def stage1_flops_per_iteration(model, mode="linear"):
         S = sum(counts)
         E = sum(counts[i] * counts[j] for i in range(n) for j in range(i + 1, n)) + S * len(p.wall_radii)
         f = (22 if mode == "linear" else 24) * E + 3 * S + 4 * n + 2 * D
+        if gradient_only:
+            f -= (2 if mode == "linear" else 3) * E + 2 * n
         if model.free_yaw:
             f += 10 * E + 8 * S
         return f
     B = p.n_blocks
     O = len(p.obstacle_radii)
-    return 22 * (B * (B - 1) // 2 + B * O) + 30 * (B - 1) + 4 * B + 2 * D
+    pairs = B * (B - 1) // 2 + B * O
+    f = 22 * pairs + 30 * (B - 1) + 4 * B + 2 * D
+    if gradient_only:
+        f -= (2 if mode == "linear" else 3) * pairs + 2 * B
+    return f
 
 
 def al_flops_per_inner_step(scene, T):
@@ -203,7 +218,9 @@ def measure_schedule_kernel(model, cfg, repeats=10):
     ms = statistics.mean(times)
     flops = cfg.m * (cfg.k_lin * stage1_flops_per_iteration(model, "linear")
                      + cfg.k_quad * stage1_flops_per_iteration(model, "quadratic"))
-    return ms, flops
+    flops_g = cfg.m * (cfg.k_lin * stage1_flops_per_iteration(model, "linear", gradient_only=True)
+                       + cfg.k_quad * stage1_flops_per_iteration(model, "quadratic", gradient_only=True))
+    return ms, flops, flops_g
 
 
 def _traffic(key):
@@ -213,9 +230,26 @@ def _traffic(key):
     return None
 
 
-def run_b200(args):
+def fp32_peak():
+    """Measured FP32 CUDA-core peak at the current clock (spasm_fp32_peak: saturating FFMA /
+    FFMA2 kernels on every SM), TFLOP/s."""
+    import ctypes
+
     import torch
 
+    from paper_2510_07674_b200 import _native as nat
+
+    out = (ctypes.c_double * 3)()
+    nat.check(nat.load().spasm_fp32_peak(ctypes.addressof(out), ctypes.addressof(out) + 8,
+                                         ctypes.addressof(out) + 16, torch.cuda.current_stream().cuda_stream),
+              "spasm_fp32_peak")
+    return {"tflops": out[0], "ffma_tflops": out[1], "ffma2_tflops": out[2]}
+
+
+def run_b200(args, workload=None, sub=False):
+    import torch
+
+    workload = workload or args.workload
     rank, world, local = dist_env()
     local = local % max(1, torch.cuda.device_count())
     if world > 1:
@@ -232,7 +266,7 @@ def run_b200(args):
 
     from paper_2510_07674_b200.sharded import TorchComm
 
-    scene_name, over, stage1_only, desc = WORKLOADS[args.workload]
+    scene_name, over, stage1_only, desc = WORKLOADS[workload]
     scene = load_scene(scene_name)
     model = as_cost_model(scene.problem, precision=args.precision)
     base = _solver_config(scene, 0, over, False)
@@ -248,7 +282,7 @@ def run_b200(args):
                            model=model, comm=comm)
 
     replan = None
-    if args.workload == "c4":
+    if workload == "c4":
         # one step = one replan tick: move the obstacle, rebuild the scene/model, re-solve
         # warm-started from the previous tick's placement (replan.py)
         from paper_2510_07674_b200.problems.scenes import tower6r
@@ -270,8 +304,10 @@ def run_b200(args):
             replan["tick_ms"].append((time.perf_counter() - t0) * 1e3)
             return sol
 
+    steps = args.sub_steps if sub else args.steps
+    warmup = args.warmup
     seed0 = 0
-    for i in range(args.warmup):
+    for i in range(warmup):
         step(seed0 + 100000 + i)
     torch.cuda.synchronize()
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")  # > 126 MB L2
@@ -281,7 +317,7 @@ def run_b200(args):
     stream = torch.cuda.current_stream()
     dev_ms, wall_ms, sols = [], [], []
     with ClockSampler(local) as clocks:
-        for i in range(args.steps):
+        for i in range(steps):
             flush.fill_(i & 0xFF)  # L2 flush between timed solves (outside the events)
             torch.cuda.synchronize()
             e0 = torch.cuda.Event(enable_timing=True)
@@ -311,7 +347,9 @@ def run_b200(args):
         launches = int(c.item())
     clk = clocks.summary()
     sm_mhz = clk["sm_mhz"] or 1965.0
-    peak = 2 * 128 * 148 * sm_mhz * 1e6 / 1e12  # FP32 CUDA-core TFLOP/s at the measured SM clock
+    nominal = 2 * 128 * 148 * sm_mhz * 1e6 / 1e12  # FP32 CUDA-core TFLOP/s at the measured SM clock
+    pk = fp32_peak()
+    peak = pk["tflops"]
     if not stage1_only and al_ms:
         T = load_scene(scene_name).trajopt_overrides.get("k_interp", 5) * (
             load_scene(scene_name).trajopt_overrides.get("k_waypoint", 1) + 1) + 1
@@ -321,27 +359,32 @@ def run_b200(args):
         roof = {"bound": "fp32", "achieved": flops / (kern_ms * 1e-3) / 1e12, "peak": peak, "unit": "TFLOP/s",
                 "kernel": "k_solve_al (persistent AL solve, CTA per trajectory particle)", "kernel_ms": kern_ms,
                 "flops_per_launch": flops, "flops_per_inner_step": f_step,
-                "traffic": _traffic(f"{args.workload}_{args.precision}_k_solve_al"),
+                "traffic": _traffic(f"{workload}_{args.precision}_k_solve_al"),
                 "note": "latency-bound: a few dozen CTAs x serial inner steps; see DESIGN.md section 3"}
     else:
-        kern_ms, flops = measure_schedule_kernel(model, base)  # one rank's m-row launch
+        kern_ms, flops, flops_g = measure_schedule_kernel(model, base)  # one rank's m-row launch
         roof = {"bound": "fp32", "achieved": flops / (kern_ms * 1e-3) / 1e12, "peak": peak, "unit": "TFLOP/s",
                 "kernel": "k_schedule (fused K_lin+K_quad descent)", "kernel_ms": kern_ms, "flops_per_launch": flops,
-                "traffic": _traffic(f"{args.workload}_{args.precision}_k_schedule")}
+                "flops_per_launch_gradient_only": flops_g,
+                "frac_gradient_only": flops_g / (kern_ms * 1e-3) / 1e12 / peak,
+                "traffic": _traffic(f"{workload}_{args.precision}_k_schedule")}
     roof["frac"] = roof["achieved"] / peak
-    roof["peak_note"] = ("FP32 CUDA-core 2*128*148*f_SM at the median SM clock sampled under load "
-                         "(MEASURED_PEAKS.json has no FP32 figure)")
+    roof["peak_nominal"] = nominal
+    roof["peak_note"] = (f"measured FP32 CUDA-core peak (spasm_fp32_peak: saturating FFMA "
+                         f"{pk['ffma_tflops']:.1f} / FFMA2 {pk['ffma2_tflops']:.1f} TFLOP/s on 148 SMs, taken after "
+                         f"the timed region; MEASURED_PEAKS.json has no FP32 figure); nominal 2*128*148*f_SM at the "
+                         f"sampled {sm_mhz:.0f} MHz is peak_nominal")
     if rank != 0:
         if world > 1:
             dist.destroy_process_group()
-        return
+        return None
     replan_line = None
     if replan is not None:
         from paper_2510_07674_b200.replan import rate_sweep
 
-        replan_line = {**rate_sweep(replan["tick_ms"][args.warmup:]), "step_m": 0.03,
-                       "warm_started_ticks": args.steps, "note": "tick = obstacle move + scene/model rebuild + solve"}
-    cpu = cpu_baseline(args) if (world == 1 and not args.no_cpu) else None
+        replan_line = {**rate_sweep(replan["tick_ms"][warmup:]), "step_m": 0.03,
+                       "warm_started_ticks": steps, "note": "tick = obstacle move + scene/model rebuild + solve"}
+    cpu = cpu_baseline(args, workload) if (world == 1 and not args.no_cpu and not sub) else None
     D = model.dimension
     p_ret = cfg.p_return
     h2d = 0 if stage1_only else p_ret * D * 8  # stage-1 placements re-enter the device for lifting
@@ -349,19 +392,20 @@ def run_b200(args):
     if not stage1_only:
         t_wp = sols[0].trajectory.segments.size if sols and sols[0].trajectory is not None else 0
         d2h += 64 + 8 * t_wp
+    ref_out = _reference_outcomes(workload, [seed0 + i for i in range(steps)], sols)
     line = {
         "metric": METRIC,
         "value": its / (total_dev * 1e-3),
         "unit": "particle-iterations/s",
         "n_gpus": world,
-        "steps": args.steps,
-        "warmup": args.warmup,
-        "ms_per_step": total_dev / args.steps,
+        "steps": steps,
+        "warmup": warmup,
+        "ms_per_step": total_dev / steps,
         # reference bench.solve_scene span: stage 1 (+ lift + AL), excluding scene load and the
         # final independent validate (bench.py:190-247); p50_step_ms is the whole timed step
         "p50_solve_ms": statistics.median(s.time_ms for s in sols),
         "p50_step_ms": statistics.median(wall_ms),
-        "success_rate": succ / args.steps,
+        "success_rate": succ / steps,
         "higher_is_better": True,
         "scaling": "weak",
         "vs_baseline": None,
@@ -381,13 +425,38 @@ def run_b200(args):
         "clocks": clk,
         "gpu_launches": launches,
         "replan": replan_line,
+        "reference_outcomes": ref_out,
         "breakdown": {"stage1_ms_mean": statistics.mean(s.stats.get("stage1_ms", 0.0) for s in sols),
                       "al_device_ms_mean": statistics.mean(al_ms) if al_ms else None,
                       "stage2_outers_mean": statistics.mean(s.stats.get("stage2_outers", 0) for s in sols)},
     }
-    print(json.dumps(line))
     if world > 1:
         dist.destroy_process_group()
+    return line
+
+
+# workload -> key prefix of the reference's own per-seed pipeline outcomes
+# (tests/golden/pipeline_reference.json, made by tests/golden/make_golden_pipeline.py)
+_REF_OUTCOME_KEYS = {"c3p": "tetris5@64k", "c2": "tower3c", "c1": "single1"}
+
+
+def _reference_outcomes(workload, seeds, sols):
+    """Per-seed success of this run next to the reference's own solve_scene on the same seeds
+    (the fixture holds the seeds the reference was run on; others are not compared)."""
+    key = _REF_OUTCOME_KEYS.get(workload)
+    path = os.path.join(ROOT, "tests", "golden", "pipeline_reference.json")
+    if key is None or not os.path.exists(path):
+        return None
+    gold = json.load(open(path))["pipeline"]
+    rows = [(seed, bool(sol.success), gold[f"{key}/{seed}"]["success"]) for seed, sol in zip(seeds, sols)
+            if f"{key}/{seed}" in gold]
+    if not rows:
+        return None
+    return {"seeds_compared": len(rows), "success_here": sum(r[1] for r in rows),
+            "success_reference": sum(r[2] for r in rows), "same_outcome": sum(r[1] == r[2] for r in rows),
+            "per_seed": [[s, int(a), int(b)] for s, a, b in rows],
+            "source": f"tests/golden/pipeline_reference.json ({key}/*: the reference's bench.solve_scene, "
+                      "variant-B fix, float64)"}
 
 
 def _oracle_solve(scene, over, stage1_only, seed, threads, max_restarts=None):
@@ -487,13 +556,13 @@ def _arm_label(threads):
     return f"oracle/pipeline.py (float64 numpy port of the reference), threads={threads}"
 
 
-def cpu_baseline(args, budget_s=20.0):
+def cpu_baseline(args, workload=None, budget_s=20.0):
     """The reference's CPU implementation (baseline/_ref when staged, else the oracle port)
     timed on this host's cores on a bounded sample of the same workload, with all host
     threads and with threads=1."""
     from paper_2510_07674_b200.problems import load_scene
 
-    scene_name, over, stage1_only, desc = WORKLOADS[args.workload]
+    scene_name, over, stage1_only, desc = WORKLOADS[workload or args.workload]
     scene = load_scene(scene_name)
     threads = os.cpu_count() or 1
     # large stage-1-only workloads: one restart per sample solve; pipelines: whole solves
@@ -568,12 +637,35 @@ def main():
     ap.add_argument("--precision", default="fp32", choices=["fp32", "fp64"])
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--no-sub", action="store_true", help="skip the C5 / C3 sub-records of the default C2 line")
+    ap.add_argument("--sub-steps", type=int, default=10, help="timed steps of each sub-record")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
         run_reference(args)
-    else:
-        run_b200(args)
+        return
+    line = run_b200(args)
+    if line is None:  # ranks != 0
+        return
+    if args.gpus == 1 and dist_env()[1] == 1 and args.workload == "c2" and not args.no_sub:
+        # same-process sub-records of the other headline configs (C5: the particle-iterations/s
+        # clause at 1M particles and k_schedule_tile's FP32 roofline; C3: 64k tetris5), each
+        # with its own clocks / roofline, so the driver's default run carries them
+        line["sub_records"] = {}
+        for w in ("c5", "c3"):
+            sub = run_b200(args, workload=w, sub=True)
+            keep = ("value", "unit", "ms_per_step", "p50_solve_ms", "p50_step_ms", "success_rate", "steps", "warmup",
+                    "config", "e2e", "roofline", "clocks", "gpu_launches", "breakdown")
+            line["sub_records"][w] = {k: sub[k] for k in keep if k in sub}
+    if args.gpus == 1 and dist_env()[1] == 1 and args.workload == "c3p" and not args.no_sub:
+        # C3's 4- and 6-object variants (stage 1 at 64k) beside the 5-object full pipeline
+        line["sub_records"] = {}
+        for w in ("c3_4", "c3_6"):
+            sub = run_b200(args, workload=w, sub=True)
+            keep = ("value", "unit", "ms_per_step", "p50_solve_ms", "p50_step_ms", "success_rate", "steps", "warmup",
+                    "config", "e2e", "roofline", "clocks", "gpu_launches", "breakdown")
+            line["sub_records"][w] = {k: sub[k] for k in keep if k in sub}
+    print(json.dumps(line))
 
 
 if __name__ == "__main__":

@@ -56,6 +56,10 @@ int64_t spasm_abi_sizeof(const char* type_name);
 /* Release the process-wide cache of pinned result-staging buffers (kept across model /
  * trajectory handles, capped at 32 buffers and 64 MB). Always SPASM_OK. */
 int spasm_trim(void);
+/* Measured FP32 CUDA-core peak (TFLOP/s) of the current device at its current clock: the
+ * larger of a saturating scalar-FFMA and a packed-FFMA2 kernel on every SM (2 flops per FMA
+ * lane). The bench's roofline denominator for the FP32 kernels. ffma / ffma2 optional. */
+int spasm_fp32_peak(double* tflops, double* ffma_tflops, double* ffma2_tflops, void* stream);
 /* Process-wide tuning switches (not in the reference; results stay within the parity
  * tolerances under every setting). "stage1_tile": -1 auto (default: on), 0 = generic
  * stage-1 kernels only, 1..4 = on (the fp32 tetris tile kernels, 4 lanes per particle;

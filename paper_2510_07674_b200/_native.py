@@ -145,6 +145,7 @@ SIGNATURES = {
     "spasm_version": (c_int, []),
     "spasm_abi_sizeof": (c_int64, [c_char_p]),
     "spasm_trim": (c_int, []),
+    "spasm_fp32_peak": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p]),
     "spasm_set_option": (c_int, [c_char_p, c_int]),
     "spasm_al_profile": (c_int, [c_int, c_void_p]),
     "spasm_tetris_model_create": (

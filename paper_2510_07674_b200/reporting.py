@@ -145,3 +145,117 @@ def read_sweep_csv(path) -> SweepGrid:
     ns = sorted({c.n for c in cells} | {n for n, _ in skipped})
     ms = sorted({c.m for c in cells} | {m for _, m in skipped})
     return SweepGrid(ns, ms, cells[0].trials if cells else 0, cells, skipped)
+
+
+# ---------------------------------------------------------------------------
+# cost traces and selection efficacy (reference bench.py:518-630)
+# ---------------------------------------------------------------------------
+def trace_solve(scene, *, seed: int = 0, threads: int = 1, solver_overrides: Optional[dict] = None,
+                quadratic_only: bool = False, precision: str = "fp64"):
+    """Cost evolution of one sampling pass, mixing selected and rejected rows
+    (bench.py:518-572): the first sampling batch of restart 0 is ranked once; the traced
+    subset is the best half of the selection plus an equal number of rejected particles
+    spread evenly over the rejected cost range; all traced rows run the full two-phase
+    schedule in ONE fused kernel launch whose device trace buffers record, after every
+    step, the cost in the active phase's mode and the QUADRATIC < epsilon flag."""
+    import numpy as np
+    import torch
+
+    from . import _native as nat
+    from .bench_api import _solver_config
+    from .particle_opt import (TRACE_PARTICLE_CAP, TraceData, _sort_indices, restart_stream, sample_uniform,
+                               torch_dtype)
+    from .problems import MotionProblem, as_cost_model
+
+    if isinstance(scene.problem, MotionProblem):
+        raise ValueError("tracing applies to placement scenes")
+    model = as_cost_model(scene.problem, precision=precision)
+    config = _solver_config(scene, seed, solver_overrides, quadratic_only)
+    batch = sample_uniform(model, config.n, restart_stream(config.seed, 0))
+    costs = model.evaluate(batch.values, "linear")
+    order = _sort_indices(costs, config.n)  # the stable ranking; its first m rows are select_topk
+    n_traced = min(config.m, TRACE_PARTICLE_CAP)
+    n_rej = min(n_traced // 2, config.n - config.m)
+    n_sel = n_traced - n_rej
+    top = order[:config.m]
+    if n_rej:
+        pool = order[config.m:]
+        pick = torch.as_tensor(np.round(np.linspace(0, len(pool) - 1, n_rej)).astype(np.int64), device=pool.device)
+        ids = torch.cat([top[:n_sel], pool[pick]])
+    else:
+        ids = top[:n_sel].clone()
+    selected = np.zeros(len(ids), dtype=bool)
+    selected[:n_sel] = True
+    steps_total = config.k_lin + config.k_quad
+    rows = ids.to(torch.int32).contiguous()
+    P = len(rows)
+    out_v = torch.empty((P, model.dimension), dtype=batch.values.dtype, device="cuda")
+    out_c = torch.empty(P, dtype=batch.values.dtype, device="cuda")
+    fl = torch.zeros(P, dtype=torch.uint8, device="cuda")
+    tc = torch.zeros((steps_total, P), dtype=torch_dtype(model.precision), device="cuda")
+    ts = torch.zeros((steps_total, P), dtype=torch.uint8, device="cuda")
+    nat.check(nat.load().spasm_descent_schedule(
+        model.handle, model.dtype_id, nat.ptr(batch.values), nat.ptr(rows), P, config.k_lin, config.k_quad,
+        config.eta_init, config.alpha, config.epsilon, nat.ptr(out_v), nat.ptr(out_c), nat.ptr(fl), None, nat.ptr(tc),
+        nat.ptr(ts), P, nat.stream_handle()), "descent_schedule (traced)")
+    return TraceData(steps=np.arange(1, steps_total + 1), particle_ids=ids.cpu().numpy().astype(np.int64),
+                     selected=selected, costs=tc.double().cpu().numpy(), satisfied=ts.cpu().numpy().astype(bool))
+
+
+def export_trace(trace, csv_path, *, svg_path=None) -> None:
+    """Write the per-step cost table, step-major (bench.py:575-589): byte-identical to the
+    reference's writer for the same TraceData."""
+    with open(csv_path, "w", newline="") as fh:
+        w = csv.writer(fh, lineterminator="\n")
+        w.writerow(["step", "particle_id", "cost", "selected", "satisfied"])
+        for si, step in enumerate(trace.steps):
+            for pi, pid in enumerate(trace.particle_ids):
+                w.writerow([int(step), int(pid), repr(float(trace.costs[si, pi])), int(trace.selected[pi]),
+                            int(trace.satisfied[si, pi])])
+    if svg_path is not None:
+        # the reference's plots.plot_trace needs matplotlib, which this image does not ship
+        import matplotlib  # noqa: F401  (raises ModuleNotFoundError exactly as the reference would)
+
+        raise NotImplementedError("SVG trace plots are out of scope (SURVEY.md section 2: plots)")
+
+
+def selection_efficacy(scene, *, trials: int = 20, seed: int = 0, threads: int = 1,
+                       solver_overrides: Optional[dict] = None, precision: str = "fp64") -> Tuple[float, float]:
+    """Satisfaction rate after the schedule: the selected top-m particles versus an
+    equal-size random subset of the rejected ones, pooled over trials (bench.py:597-630).
+
+    Sampling, ranking, the fused schedule and the satisfaction test run on the GPU. The
+    rejected subset is the reference's ``rng.choice(pool, m, replace=False)`` on the
+    restart stream continued past the batch draw: numpy's own Generator on the same
+    SeedSequence state advanced by the n*D doubles the uniform draw consumed, so the subset
+    is the reference's exactly."""
+    import numpy as np
+    import torch
+
+    from .bench_api import _solver_config
+    from .particle_opt import _sort_indices, restart_stream, run_descent_schedule, sample_uniform
+    from .problems import MotionProblem, as_cost_model
+
+    if isinstance(scene.problem, MotionProblem):
+        raise ValueError("placement scenes only")
+    model = as_cost_model(scene.problem, precision=precision)
+    sel_hits = rej_hits = total = 0
+    for i in range(trials):
+        config = _solver_config(scene, seed + i, solver_overrides, False)
+        if config.n - config.m < config.m:
+            raise ValueError("need n >= 2*m to draw the rejected subset")
+        batch = sample_uniform(model, config.n, restart_stream(config.seed, 0))
+        costs = model.evaluate(batch.values, "linear")
+        top = _sort_indices(costs, config.m)
+        rng = np.random.default_rng(np.random.SeedSequence(entropy=config.seed, spawn_key=(0,)))
+        rng.bit_generator.advance(config.n * model.dimension)
+        pool = np.setdiff1d(np.arange(config.n), top.cpu().numpy())
+        rejected = torch.as_tensor(rng.choice(pool, size=config.m, replace=False), device="cuda")
+        values = torch.cat([batch.values[top], batch.values[rejected]])
+        run_descent_schedule(model, values, config, threads=threads)
+        sat = model.satisfaction(values, config.epsilon)
+        sat = sat.cpu().numpy() if hasattr(sat, "cpu") else np.asarray(sat)
+        sel_hits += int(np.count_nonzero(sat[:config.m]))
+        rej_hits += int(np.count_nonzero(sat[config.m:]))
+        total += config.m
+    return sel_hits / total, rej_hits / total

@@ -40,6 +40,9 @@ sys.path.insert(0, ROOT)
 
 # (scene, seeds of the full pipeline)
 PIPELINE = {"single1": range(5), "tower4": range(5), "tower3c": range(5), "tetris5": range(10)}
+# BASELINE C3 at its stated size (64k particles, M = 8192) through the full pipeline:
+# key -> (scene, solver overrides, seeds)
+PIPELINE_SIZED = {"tetris5@64k": ("tetris5", {"n": 65536, "m": 8192}, range(10))}
 # stage-1-only configs (scenes without a robot, or no_trajopt): seeds 0..19
 STAGE1 = ["single1", "tower4", "tower3c", "tower6r", "tetris4", "tetris5", "tetris6"]
 STAGE1_SEEDS = range(20)
@@ -81,12 +84,20 @@ def main():
 
     bench.solve, bench.lift_placements, bench.solve_al = w_solve, w_lift, w_al
 
+    path = os.path.join(HERE, "pipeline_reference.json")
+    only = sys.argv[1:]  # optional: regenerate just these keys (e.g. tetris5@64k), merged into the file
     out = {"pipeline": {}, "stage1": {}}
-    for name, seeds in PIPELINE.items():
+    if only and os.path.exists(path):
+        out = json.load(open(path))
+    cases = [(name, name, {}, seeds) for name, seeds in PIPELINE.items()]
+    cases += [(key, name, over, seeds) for key, (name, over, seeds) in PIPELINE_SIZED.items()]
+    for key, name, over, seeds in cases:
+        if only and key not in only:
+            continue
         scene = ref_scene(name)
         for seed in seeds:
             rec.clear()
-            sol = bench.solve_scene(scene, seed=seed)
+            sol = bench.solve_scene(scene, seed=seed, solver_overrides=over or None)
             s1 = rec["stage1"]
             entry = {"success": bool(sol.success), "restarts": int(sol.restarts),
                      "stage1_success": bool(s1.success), "stage1_indices": [int(i) for i in s1.indices],
@@ -97,10 +108,12 @@ def main():
                      "al_particle": int(rec["al"].particle_index) if "al" in rec else -1,
                      "objective": float(rec["al"].objective) if "al" in rec else None,
                      "least_violation": float(rec["al_fail"].best_violation) if "al_fail" in rec else None}
-            out["pipeline"][f"{name}/{seed}"] = entry
-            print(name, seed, {k: v for k, v in entry.items() if k not in ("stage1_indices", "stage1_costs", "kept")},
+            out["pipeline"][f"{key}/{seed}"] = entry
+            print(key, seed, {k: v for k, v in entry.items() if k not in ("stage1_indices", "stage1_costs", "kept")},
                   flush=True)
     for name in STAGE1:
+        if only and name not in only:
+            continue
         scene = ref_scene(name)
         for seed in STAGE1_SEEDS:
             rec.clear()
@@ -111,7 +124,6 @@ def main():
                 "stage1_indices": [int(i) for i in s1.indices], "stage1_costs": [float(c) for c in s1.costs]}
         print(name, "stage1", sum(v["success"] for k, v in out["stage1"].items() if k.startswith(name + "/")),
               "successes", flush=True)
-    path = os.path.join(HERE, "pipeline_reference.json")
     with open(path, "w") as f:
         json.dump(out, f, indent=0, sort_keys=True)
     print("wrote", path)

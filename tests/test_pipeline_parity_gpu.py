@@ -53,12 +53,17 @@ CHAOTIC = {"tower3c/0": (1e-4, 0.1), "tower4/3": (1e-5, 1e-4), "tower4/4": (5e-3
            "tetris5/3": (1e-6, 5e-4), "tetris5/5": (1e-6, 1e-4)}
 
 
+# sized cases: BASELINE C3 at its stated size (make_golden_pipeline.PIPELINE_SIZED)
+SIZED = {"tetris5@64k": {"n": 65536, "m": 8192}}
+
+
 @pytest.mark.parametrize("case", PIPE)
 def test_fp64_pipeline_matches_reference(case):
-    name, seed = case.split("/")
+    key, seed = case.split("/")
+    name = key.split("@")[0]
     ref = GOLD["pipeline"][case]
     scene, model = _model(name, "fp64")
-    sol = solve_scene(scene, seed=int(seed), model=model, precision="fp64")
+    sol = solve_scene(scene, seed=int(seed), model=model, precision="fp64", solver_overrides=SIZED.get(key))
     bk = sol.bookkeeping
     assert sol.success == ref["success"], (case, sol.success, ref["success"], sol.max_violation)
     assert sol.restarts == ref["restarts"]
