@@ -1,20 +1,27 @@
 // The augmented-Lagrangian engine of stage 2, one CTA per trajectory particle.
 //
 // Thread mapping: one 8-lane tile per waypoint w = (segment b, step t), lane j = joint j
-// (W = B*T tiles), plus one auxiliary warp for per-segment work. Per inner step:
+// (W = B*T tiles), plus one auxiliary warp for per-segment work. One inner step is two
+// CTA-wide barriers; the phases between them overlap:
 //
-//   P1 tiles: tile FK of the waypoint (coop.cuh), arm-sphere centres of link j on lane j,
-//             held-block spheres round-robin over lanes, path-length leg, start terms.
-//   P2 tiles: penetrations vs the segment's fixed obstacles (statics + later staged blocks).
-//      aux:   placed block poses from the final waypoints, then the free-yaw placement
-//             twin's cost + gradient (trajopt.py:448-472, 531-539), overlapping P2.
-//   P3 tiles: penetrations vs earlier placed blocks, their placed-pose partials (tile
-//             reduced), Jacobian-transpose products: lane k gets
+//   A  aux:   tile FK of the B final waypoints (4 tiles per warp), placed block poses
+//             (trajopt.py:448-472) -> arrive at named barrier kBarPlaced; then the
+//             free-yaw placement twin's cost + gradient (trajopt.py:281-302, 531-539).
+//      tiles: P1 tile FK of the waypoint (coop.cuh), arm-sphere centres of link j on lane
+//             j, held-block spheres round-robin over lanes; sync kBarPlaced (only the
+//             placed poses cross warps); P2 path-length leg, start terms, penetrations vs
+//             the segment's fixed obstacles (statics + later staged blocks); P3 penetrations
+//             vs earlier placed blocks, their placed-pose partials (tile reduced),
+//             Jacobian-transpose products: lane k gets
 //             z_k . (sum_{link>=k} a x g - o_k x sum_{link>=k} g) from a suffix scan.
-//   P4       totals, constraint vector, multiplier scales; aux reduces placed partials.
-//   P5 tiles: lane k assembles dL/dq_k (path length, arm, held, placement chain through the
-//             final-waypoint Jacobian and exact yaw Jacobian, start alignment) and either
-//             stores it or applies the clamped descent step in place.
+//   -- __syncthreads --
+//   B  every tile lane forms the totals, constraint vector and multiplier scales itself
+//      (same operands, same order: identical bits on every lane); the final-waypoint tiles
+//      sum their segment's placed-pose partials; lane k assembles dL/dq_k (path length,
+//      arm, held, placement chain through the final-waypoint Jacobian and exact yaw
+//      Jacobian, start alignment) and either stores it or applies the clamped descent
+//      step in place.
+//   -- __syncthreads --
 //
 // Reductions run in a fixed order (xor trees, ordered loops; no atomics): deterministic.
 // Reference: trajopt.py:396-653 (value + gradient), 936-1063 (solve), 1071-1153 (validate).
@@ -123,6 +130,14 @@ struct AlProf {
     }
   }
 };
+
+// named barrier 2: the aux warp arrives once the placed poses are written, the tile warps
+// sync on it before their first read of them (every warp converged at the call)
+constexpr int kBarPlaced = 2;
+__device__ __forceinline__ void bar_placed_arrive(int count) {
+  asm volatile("bar.arrive 2, %0;" ::"r"(count) : "memory");
+}
+__device__ __forceinline__ void bar_placed_sync(int count) { asm volatile("bar.sync 2, %0;" ::"r"(count) : "memory"); }
 
 template <typename R>
 struct AlCtx {
@@ -233,14 +248,15 @@ __device__ void al_eval(AlCtx<R>& C, const typename TwinSceneOf<R, KIND>::type& 
   const TrajScene<R>& sc = *C.sc;
   const ChainDesc<R>& ch = sc.ch;
   const int tid = threadIdx.x;
-  const int W = C.L.W, J = ch.J, T = prm.T, B = sc.B, S = ch.S, SBn = C.L.SB;
+  // sizes from the kernel-parameter layout (uniform to the compiler; equal to the scene's)
+  const int W = C.L.W, J = C.L.J, T = prm.T, B = C.L.B, S = C.L.S, SBn = C.L.SB;
   const bool manip = sc.manip != 0;
   const bool is_aux = tid >= C.L.NW;
   const int lane = tid & 31;
   const int w = tid >> 3;
   const bool is_wp = !is_aux && w < W;
   const Tile tl = Tile::make();
-  const Tile tlw = Tile::make_warp();  // for the calls every lane of the tile warps reaches
+  const Tile tlw = Tile::make_warp();  // for the calls every lane of the warp reaches
   const int j = tl.j;
   const int b = is_wp ? w / T : 0;
   const int t = is_wp ? w - b * T : 0;
@@ -249,75 +265,54 @@ __device__ void al_eval(AlCtx<R>& C, const typename TwinSceneOf<R, KIND>::type& 
   const int nh = manip ? sc.blk_start[b + 1] - h0 : 0;
   const int f0 = manip ? sc.blk_start[b + 1] : 0, f1 = manip ? sc.n_blk : 0;
   const R w_start = R(prm.w_start);
+  const int bar_count = C.L.NW + 32;
   WpState<R> st;
   R obj_w = R(0), carm = R(0), cblk = R(0);
   // tower twin helpers (twin_warp.cuh): the last two tile warps take the stability
   // supports and the cube-obstacle pairs
   const int twin_ext = KIND == 2 ? (C.L.NW >= 64 ? 2 : 1) : 0;
 
-  // ---------------- P1: tile FK, sphere centres, placed poses ----------------------------
-  if (!is_aux && w < C.L.NW / kTile) {
-    const int wq = is_wp ? w : 0;  // padding tiles mirror waypoint 0 (no writes)
-    const R qj = j < J ? C.x[wq * kXS + j] : R(0);
-    TileFrame<R> f;
-    tile_fk(tlw, ch, qj, f);
-#pragma unroll
-    for (int c = 0; c < 3; ++c) {
-      st.z[c] = f.z[c];
-      st.o[c] = f.o[c];
-      st.ee[c] = f.ee[c];
-    }
-#pragma unroll
-    for (int c = 0; c < 9; ++c) st.Ree[c] = f.Ree[c];
-    if (is_wp) {
-      if (j == 0) {
-#pragma unroll
-        for (int c = 0; c < 3; ++c) C.ee[w * 3 + c] = f.ee[c];
-#pragma unroll
-        for (int c = 0; c < 9; ++c) C.rot[w * 9 + c] = f.Ree[c];
-      }
-      if (manip && t == T - 1) {  // placed pose from the final waypoint (trajopt.py:448-472)
-        const R ps = yaw_of(f.Ree) - sc.grasp_yaw;
-        R s, c;
-        Math<R>::sincos_(ps, &s, &c);
-        if (j == 0) {
-          const R ox = sc.grasp_off[0], oy = sc.grasp_off[1], oz = sc.grasp_off[2];
-          C.psi[b] = ps;
-          C.cp[b] = c;
-          C.sp[b] = s;
-          C.rows[4 * b + 0] = f.ee[0] - (c * ox - s * oy);
-          C.rows[4 * b + 1] = f.ee[1] - (s * ox + c * oy);
-          C.rows[4 * b + 2] = f.ee[2] - oz;
-          C.rows[4 * b + 3] = ps;
-        }
-        for (int q = sc.blk_start[b] + j; q < sc.blk_start[b + 1]; q += kTile) {
-          const R ux = sc.bu[q][0], uy = sc.bu[q][1], uz = sc.bu[q][2];
-          C.pl[3 * q + 0] = f.ee[0] + c * ux - s * uy;
-          C.pl[3 * q + 1] = f.ee[1] + s * ux + c * uy;
-          C.pl[3 * q + 2] = f.ee[2] + uz;
-        }
-      }
-      if (j < J)
-        for (int s = ch.link_start[j]; s < ch.link_start[j + 1]; ++s) tile_sphere(ch, f, s, C.armw + (w * S + s) * 3);
-      if (interior) {  // held block = Ree @ FLIP @ u + ee (trajopt.py:441-447)
-        for (int s = j; s < nh; s += kTile) {
-          const R ux = sc.bu[h0 + s][0], uy = sc.bu[h0 + s][1], uz = sc.bu[h0 + s][2];
-          R* h = C.hp + (w * SBn + s) * 3;
-          h[0] = ((f.Ree[0] * ux - f.Ree[1] * uy) - f.Ree[2] * uz) + f.ee[0];
-          h[1] = ((f.Ree[3] * ux - f.Ree[4] * uy) - f.Ree[5] * uz) + f.ee[1];
-          h[2] = ((f.Ree[6] * ux - f.Ree[7] * uy) - f.Ree[8] * uz) + f.ee[2];
-        }
-      }
-    }
-  }
-  C.prof.arrive(0, C.L.NW);
-  __syncthreads();
-  C.prof.mark(0);
-
-  // ---------------- P2: aux = placement twin (placed poses came from P1); tiles = fixed
-  // obstacles
-  if (is_aux) {
+  // warp-role predicates from a warp vote: uniform by construction, so ptxas can branch on
+  // them without divergence handling and the warp-wide shuffles inside stay plain SHFLs
+  const bool aux_warp = __all_sync(0xffffffffu, is_aux);
+  if (aux_warp) {
+    // ================= phase A, aux warp ==================================================
     if (manip) {
+      // placed poses from the final waypoints: the aux warp runs the B final-waypoint FKs
+      // itself (4 tiles of 8 lanes, uniform trip count) so no tile waits for another warp's
+      // FK; identical frames to the waypoint tiles' (same code, same operands)
+      const int sub = lane >> 3;
+      for (int base = 0; base < B; base += 4) {
+        const int bb = base + sub;
+        const bool act = bb < B;
+        const int wf = (act ? bb : 0) * T + T - 1;
+        const R qj = j < J ? C.x[wf * kXS + j] : R(0);
+        TileFrame<R> f;
+        tile_fk(tlw, ch, qj, f);
+        if (act) {
+          const R ps = yaw_of(f.Ree) - sc.grasp_yaw;
+          R s, c;
+          Math<R>::sincos_(ps, &s, &c);
+          if (j == 0) {
+            const R ox = sc.grasp_off[0], oy = sc.grasp_off[1];
+            C.psi[bb] = ps;
+            C.cp[bb] = c;
+            C.sp[bb] = s;
+            C.rows[4 * bb + 0] = f.ee[0] - (c * ox - s * oy);
+            C.rows[4 * bb + 1] = f.ee[1] - (s * ox + c * oy);
+            C.rows[4 * bb + 2] = f.ee[2] - sc.grasp_off[2];
+            C.rows[4 * bb + 3] = ps;
+          }
+          for (int q = sc.blk_start[bb] + j; q < sc.blk_start[bb + 1]; q += kTile) {
+            const R ux = sc.bu[q][0], uy = sc.bu[q][1], uz = sc.bu[q][2];
+            C.pl[3 * q + 0] = f.ee[0] + c * ux - s * uy;
+            C.pl[3 * q + 1] = f.ee[1] + s * ux + c * uy;
+            C.pl[3 * q + 2] = f.ee[2] + uz;
+          }
+        }
+      }
+      __syncwarp();
+      bar_placed_arrive(bar_count);
       if (C.prof.on && lane == 0) atomicAdd(&g_al_arrive[1][5], (unsigned long long)(clock64() - C.prof.t));
       R cpl = twin_warp<R, KIND, SPB>(tw, C.rows, C.gpose, C.scr, lane, want_grad, pquad, twin_ext);
       if (C.prof.on && lane == 0) atomicAdd(&g_al_arrive[1][6], (unsigned long long)(clock64() - C.prof.t));
@@ -332,9 +327,50 @@ __device__ void al_eval(AlCtx<R>& C, const typename TwinSceneOf<R, KIND>::type& 
       }
       if (lane == 0) C.scal[kCplace] = cpl;
     }
-  } else if (w < C.L.NW / kTile) {
-    // tower scenes: the last tile warps run parts of the twin first, handing them to the
-    // aux warp at named barrier 1 (the twin bounds this phase)
+  } else {
+    // ================= phase A, waypoint tiles ============================================
+    // ---- P1: tile FK, sphere centres
+    const int wq = is_wp ? w : 0;  // padding tiles mirror waypoint 0 (no writes)
+    const R qj = j < J ? C.x[wq * kXS + j] : R(0);
+    {
+      TileFrame<R> f;
+      tile_fk(tlw, ch, qj, f);
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        st.z[c] = f.z[c];
+        st.o[c] = f.o[c];
+        st.ee[c] = f.ee[c];
+      }
+#pragma unroll
+      for (int c = 0; c < 9; ++c) st.Ree[c] = f.Ree[c];
+      if (is_wp) {
+        if (j == 0) {
+#pragma unroll
+          for (int c = 0; c < 3; ++c) C.ee[w * 3 + c] = f.ee[c];
+#pragma unroll
+          for (int c = 0; c < 9; ++c) C.rot[w * 9 + c] = f.Ree[c];
+        }
+        if (j < J)
+          for (int s = ch.link_start[j]; s < ch.link_start[j + 1]; ++s) tile_sphere(ch, f, s, C.armw + (w * S + s) * 3);
+        if (interior) {  // held block = Ree @ FLIP @ u + ee (trajopt.py:441-447)
+          for (int s = j; s < nh; s += kTile) {
+            const R ux = sc.bu[h0 + s][0], uy = sc.bu[h0 + s][1], uz = sc.bu[h0 + s][2];
+            R* h = C.hp + (w * SBn + s) * 3;
+            h[0] = ((f.Ree[0] * ux - f.Ree[1] * uy) - f.Ree[2] * uz) + f.ee[0];
+            h[1] = ((f.Ree[3] * ux - f.Ree[4] * uy) - f.Ree[5] * uz) + f.ee[1];
+            h[2] = ((f.Ree[6] * ux - f.Ree[7] * uy) - f.Ree[8] * uz) + f.ee[2];
+          }
+        }
+      }
+    }
+    C.prof.arrive(0, C.L.NW);
+    // the placed poses (aux warp) are the only cross-warp input of P2/P3; the sync also
+    // orders this warp's own P1 writes (held spheres are read by other lanes below)
+    if (manip) bar_placed_sync(bar_count);
+    else __syncwarp();
+    C.prof.mark(0);
+
+    // ---- P2: tower twin helper parts, leg, start terms, fixed obstacles
     if constexpr (KIND == 2) {
       // 2 (stability) = last tile warp (the lightest: padding tiles), 1 (cube-obstacle
       // pairs) = the one before it; with a single tile warp it takes part 1
@@ -342,10 +378,6 @@ __device__ void al_eval(AlCtx<R>& C, const typename TwinSceneOf<R, KIND>::type& 
       const int part = twin_ext == 2 ? 3 - back : back;
       if (manip && back <= twin_ext) twin_tower_helper<R>(tw, C.rows, C.scr, lane, want_grad, pquad, part, twin_ext);
     }
-    // path length and start alignment moved here from P1: the tile warps have slack in P2
-    // (the aux warp's placement twin bounds it), so P1 ends sooner
-    const int wq = is_wp ? w : 0;
-    const R qj = j < J ? C.x[wq * kXS + j] : R(0);
     // path length (trajopt.py:474-476): tile sum of the leg's squared components
     R dv = R(0);
     if (is_wp && t < T - 1 && j < J) dv = C.x[(wq + 1) * kXS + j] - qj;
@@ -372,7 +404,7 @@ __device__ void al_eval(AlCtx<R>& C, const typename TwinSceneOf<R, KIND>::type& 
     }
     // Sphere-major: the tile's 8 lanes take the waypoint's spheres (arm spheres, then the
     // held-block spheres) round-robin, each against the whole fixed list, so a sphere's
-    // gradient stays lane-local (no tile sums) and the values join the warp sums of P3.
+    // gradient stays lane-local (no tile sums) and the values join the warp sums below.
     if (is_wp) {
       const int n_items = S + (interior ? nh : 0);
       for (int it = j; it < n_items; it += kTile) {
@@ -389,15 +421,13 @@ __device__ void al_eval(AlCtx<R>& C, const typename TwinSceneOf<R, KIND>::type& 
         else cblk += v;
       }
     }
-  }
-  C.prof.arrive(1, C.L.NW);
-  __syncthreads();
-  C.prof.mark(1);
+    C.prof.arrive(1, C.L.NW);
+    __syncwarp();  // P3 reads the sphere gradients other lanes of the tile wrote
+    C.prof.mark(1);
 
-  // ---------------- P3: placed blocks, placed-pose partials, J^T products ------------------
-  st.garm = R(0);
-  st.gblk = R(0);
-  if (!is_aux && w < C.L.NW / kTile) {
+    // ---- P3: placed blocks, placed-pose partials, J^T products
+    st.garm = R(0);
+    st.gblk = R(0);
     if (manip) {
       // uniform trip count over the warp (blocks jb < B - 1; a waypoint of segment b uses
       // jb < b) so the partial sums below can use the warp-mask shuffles
@@ -508,9 +538,7 @@ __device__ void al_eval(AlCtx<R>& C, const typename TwinSceneOf<R, KIND>::type& 
       cross3(st.o, Gh, og);
       st.gblk = (st.z[0] * (Mh[0] - og[0]) + st.z[1] * (Mh[1] - og[1])) + st.z[2] * (Mh[2] - og[2]);
     }
-  }
-  // warp partial sums of the scalars (fixed xor-tree order)
-  if (!is_aux) {
+    // warp partial sums of the scalars (fixed xor-tree order)
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) {
       obj_w += __shfl_xor_sync(0xffffffffu, obj_w, off);
@@ -522,13 +550,18 @@ __device__ void al_eval(AlCtx<R>& C, const typename TwinSceneOf<R, KIND>::type& 
       C.red[4 * (tid >> 5) + 1] = carm;
       C.red[4 * (tid >> 5) + 2] = cblk;
     }
+    C.prof.arrive(2, C.L.NW);
   }
-  C.prof.arrive(2, C.L.NW);
   __syncthreads();
   C.prof.mark(2);
 
-  // ---------------- P4: totals, multiplier scales; aux reduces placed partials ----------
-  if (tid == 0) {
+  // ================= phase B ==============================================================
+  // totals, constraint vector and multiplier scales (trajopt.py:541-548): formed by thread
+  // 0 for the records and, redundantly, by every lane that assembles a gradient (same
+  // operands in the same order: bitwise identical), so no further barrier is needed
+  const bool grad_lane = want_grad && is_wp && j < J;
+  R s_pl = R(0), s_arm = R(0), s_blk = R(0);
+  if (tid == 0 || grad_lane) {
     R o = R(0), ca = R(0), cb = R(0);
     for (int wi = 0; wi < C.L.NW / 32; ++wi) {
       o += C.red[4 * wi];
@@ -539,45 +572,34 @@ __device__ void al_eval(AlCtx<R>& C, const typename TwinSceneOf<R, KIND>::type& 
     const R c0 = R(prm.w_place) * cpl, c1 = R(prm.w_arm) * ca, c2 = R(prm.w_block) * cb;
     const R mu = C.scal[kMu];
     const R l0 = C.scal[kLam0], l1 = C.scal[kLam1], l2 = C.scal[kLam2];
-    C.scal[kObj] = o;
-    C.scal[kCarm] = ca;
-    C.scal[kCblk] = cb;
-    C.scal[kCons0] = c0;
-    C.scal[kCons1] = c1;
-    C.scal[kCons2] = c2;
-    C.scal[kLag] = o + ((l0 * c0 + l1 * c1) + l2 * c2) + R(0.5) * mu * ((c0 * c0 + c1 * c1) + c2 * c2);
-    C.scal[kSc0] = (l0 + mu * c0) * R(prm.w_place);
-    C.scal[kSc1] = (l1 + mu * c1) * R(prm.w_arm);
-    C.scal[kSc2] = (l2 + mu * c2) * R(prm.w_block);
-  }
-  // placed-block partials summed over the later segments' waypoints (waypoint order per
-  // quarter, quarters combined (q0 + q1) + (q2 + q3)): 4 lanes per item on the tile warps
-  // other than warp 0 (thread 0 forms the totals above); the aux warp when there is none
-  if (want_grad && manip) {
-    const int total = 32 * B;  // 8B items x 4 quarters
-    const bool tiles = C.L.NW >= 64;
-    if (tiles ? (!is_aux && tid >= 32) : is_aux) {
-      const int first = tiles ? ((tid - 32) & ~31) : 0, stride = tiles ? C.L.NW - 32 : 32;
-      for (int u0 = first; u0 < total; u0 += stride) {  // warp-uniform trip count
-        const int u = u0 + lane, it = u >> 2, part = u & 3;
-        R s = R(0);
-        if (u < total) {
-          const int cls = it / (4 * B), jb = (it / 4) % B, i = it % 4;
-          for (int wv = (jb + 1) * T + part; wv < W; wv += 4) s += C.pg[((wv * 2 + cls) * B + jb) * 4 + i];
-        }
-        s += __shfl_xor_sync(0xffffffffu, s, 1);
-        s += __shfl_xor_sync(0xffffffffu, s, 2);
-        if (u < total && part == 0) C.pgsum[it] = s;
-      }
+    s_pl = (l0 + mu * c0) * R(prm.w_place);
+    s_arm = (l1 + mu * c1) * R(prm.w_arm);
+    s_blk = (l2 + mu * c2) * R(prm.w_block);
+    if (tid == 0) {
+      C.scal[kObj] = o;
+      C.scal[kCarm] = ca;
+      C.scal[kCblk] = cb;
+      C.scal[kCons0] = c0;
+      C.scal[kCons1] = c1;
+      C.scal[kCons2] = c2;
+      C.scal[kLag] = o + ((l0 * c0 + l1 * c1) + l2 * c2) + R(0.5) * mu * ((c0 * c0 + c1 * c1) + c2 * c2);
+      C.scal[kSc0] = s_pl;
+      C.scal[kSc1] = s_arm;
+      C.scal[kSc2] = s_blk;
     }
   }
-  C.prof.arrive(3, C.L.NW);
-  __syncthreads();
-  C.prof.mark(3);
+  // placed-block partials of segment b summed over the later segments' waypoints, in
+  // waypoint order, by its final-waypoint tile: lane j forms item j ([class j/4][xyz|yaw])
+  if (want_grad && manip && is_wp && t == T - 1) {
+    const int cls = j >> 2, i = j & 3;
+    R sum = R(0);
+    for (int wv = (b + 1) * T; wv < W; ++wv) sum += C.pg[((wv * 2 + cls) * B + b) * 4 + i];
+    C.pgsum[(cls * B + b) * 4 + i] = sum;
+    __syncwarp(tl.mask);
+  }
 
-  // ---------------- P5: gradient assembly (lane k = joint k) + optional update -----------
-  if (want_grad && is_wp && j < J) {
-    const R s_pl = C.scal[kSc0], s_arm = C.scal[kSc1], s_blk = C.scal[kSc2];
+  // gradient assembly (lane k = joint k) + optional update
+  if (grad_lane) {
     R gq = R(0);
     if (t < T - 1) gq -= C.unit[w * kXS + j];
     if (t >= 1) gq += C.unit[(w - 1) * kXS + j];
@@ -638,7 +660,8 @@ __device__ void al_validate(AlCtx<R>& C, const typename TwinSceneOf<R, KIND>::ty
   const TrajScene<R>& sc = *C.sc;
   const ChainDesc<R>& ch = sc.ch;
   const int tid = threadIdx.x;
-  const int W = C.L.W, J = ch.J, T = prm.T, B = sc.B, S = ch.S, SBn = C.L.SB;
+  // sizes from the kernel-parameter layout (uniform to the compiler; equal to the scene's)
+  const int W = C.L.W, J = C.L.J, T = prm.T, B = C.L.B, S = C.L.S, SBn = C.L.SB;
   const bool manip = sc.manip != 0;
   const bool is_aux = tid >= C.L.NW;
   const int lane = tid & 31;
@@ -906,8 +929,8 @@ __global__ void __launch_bounds__(kMaxAlThreads) k_solve_al(const TrajScene<R>* 
     // retract pick waypoints to the exact grasp (trajopt.py:1004-1007), lane j = joint j.
     // With at least B tile warps, warp bb polishes segment bb as 4 identical 8-lane replicas
     // (warp-mask shuffles, replicas exit together); else one tile per segment.
-    if (manip && L.NW / 32 >= sc.B) {
-      if ((tid >> 5) < sc.B) {
+    if (manip && L.NW / 32 >= L.B) {
+      if (__all_sync(0xffffffffu, (tid >> 5) < L.B)) {  // warp-uniform (vote): plain shuffles inside
         const Tile tlw = Tile::make_warp();
         const int bb = tid >> 5;
         const int w0 = bb * T;
@@ -916,7 +939,7 @@ __global__ void __launch_bounds__(kMaxAlThreads) k_solve_al(const TrajScene<R>* 
         __syncwarp();  // the replica lanes' reads of x above precede lanes 0-7's writes
         if ((tid & 31) < kTile && tlw.j < J) C.x[w0 * kXS + tlw.j] = qj;
       }
-    } else if (manip && (tid >> 3) < sc.B) {
+    } else if (manip && (tid >> 3) < L.B) {
       const Tile tl = Tile::make();
       const int bb = tid >> 3;
       const int w0 = bb * T;

@@ -67,6 +67,11 @@ struct Tile {
     for (int k = 0; k < 2; ++k) b[k] = (h1 ? a[k + 2] : a[k]) + xr(h1 ? a[k] : a[k + 2], 2);
     return (h0 ? b[1] : b[0]) + xr(h0 ? b[0] : b[1], 1);
   }
+  // tile-uniform predicate (the loop exits below are uniform across the tile; with the
+  // warp mask the vote also makes them uniform to the compiler, so the loops' warp-wide
+  // shuffles need no divergence handling)
+  __device__ __forceinline__ bool all(bool p) const { return __all_sync(mask, p); }
+  __device__ __forceinline__ bool any(bool p) const { return __any_sync(mask, p); }
   template <typename R>
   __device__ __forceinline__ R max(R v) const {
     v = fmax(v, xr(v, 1));
@@ -262,7 +267,7 @@ __device__ bool tile_ik(const Tile& tl, const ChainDesc<R>& ch, R& qj, const R t
     const R pe[3] = {tp[0] - f.ee[0], tp[1] - f.ee[1], tp[2] - f.ee[2]};
     const R ye = wrap_yaw(ty - yaw_of(f.Ree));
     const R pn = Math<R>::sqrt_((pe[0] * pe[0] + pe[1] * pe[1]) + pe[2] * pe[2]);
-    if (pn < R(kIkPosTol) && fabs(ye) < R(kIkYawTol)) break;
+    if (tl.all(pn < R(kIkPosTol) && fabs(ye) < R(kIkYawTol))) break;
     const R rel[3] = {f.ee[0] - f.o[0], f.ee[1] - f.o[1], f.ee[2] - f.o[2]};
     R c[3];
     cross3(f.z, rel, c);
@@ -308,14 +313,15 @@ __device__ bool tile_polish(const Tile& tl, const ChainDesc<R>& ch, R& qj, const
         const int b = *best;
         stop = (b >= 0) ? (b != me) : (cur != nullptr && *cur != mine);
       }
-      if (__shfl_sync(tl.mask, stop, 0, kTile)) return false;
+      // any replica's lane 0 seeing the stop condition stops the whole tile / warp together
+      if (tl.any(stop != 0)) return false;
     }
     tile_fk(tl, lc, qj, f);
     const R pe[3] = {tp[0] - f.ee[0], tp[1] - f.ee[1], tp[2] - f.ee[2]};
     const R ye = wrap_yaw(ty - yaw_of(f.Ree));
     const R ax[3] = {f.Ree[2], f.Ree[5], f.Ree[8]};
     const R pn = Math<R>::sqrt_((pe[0] * pe[0] + pe[1] * pe[1]) + pe[2] * pe[2]);
-    if (pn < R(kIkPosTol) && fabs(ye) < R(kIkYawTol) && -ax[2] > cos_tol) break;
+    if (tl.all(pn < R(kIkPosTol) && fabs(ye) < R(kIkYawTol) && -ax[2] > cos_tol)) break;
     const R rel[3] = {f.ee[0] - f.o[0], f.ee[1] - f.o[1], f.ee[2] - f.o[2]};
     R c[3], d[3];
     cross3(f.z, rel, c);

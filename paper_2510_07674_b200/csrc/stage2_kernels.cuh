@@ -116,7 +116,9 @@ __global__ void __launch_bounds__(MAXT) k_ik_group(const TrajScene<R>* __restric
   R qj = R(0);
   bool pol_spec = true, spec_done = false;
   R ik_q = R(0);
-  if (tile < restarts) {
+  // warp-uniform role predicates from votes (uniform to the compiler: the warp-wide tile
+  // shuffles inside need no divergence handling)
+  if (__all_sync(0xffffffffu, tile < restarts)) {
     if (tl.j < J) {
       // seeds[t] = uniform(lower, upper, (restarts, dof)) of SeedSequence(seed, (t,)) (robot.py:255-257)
       Pcg64 g;
@@ -152,10 +154,11 @@ __global__ void __launch_bounds__(MAXT) k_ik_group(const TrajScene<R>* __restric
     // its IK result at once and stops if a better one finishes or another tile wins, so
     // the winner's polish usually overlaps the slower restarts' IK iterations
     ik_q = qj;
-    if (polish && lead) pol_spec = tile_polish<R>(tl, ch, qj, tp, ty, &s_best, tile, &s_cur, mine, &spec_done);
+    if (polish && __all_sync(0xffffffffu, lead != 0))
+      pol_spec = tile_polish<R>(tl, ch, qj, tp, ty, &s_best, tile, &s_cur, mine, &spec_done);
   }
   __syncthreads();
-  if (tile != s_best) return;  // the whole winner warp stays: the polish below shuffles warp-wide
+  if (!__all_sync(0xffffffffu, tile == s_best)) return;  // the whole winner warp stays: its polish shuffles warp-wide
   bool pol = true;
   R pen = R(0);
   if (polish) {

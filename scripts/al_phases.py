@@ -23,8 +23,8 @@ for s in range(solves):
     sol = solve_scene(scene, seed=s, model=model)
     outers += sol.stats.get("stage2_outers", 0)
 lib.spasm_al_profile(0, out.ctypes.data)
-names = {0: "P1 FK/spheres/leg/start", 1: "P2 fixed obstacles + twin", 2: "P3 placed blocks + J^T",
-         3: "P4 totals/scales", 4: "P5 assemble + step", 8: "pick polish", 9: "re-eval + validate"}
+names = {0: "A/P1 FK/spheres (+ placed-pose sync)", 1: "A/P2 leg/start/fixed obstacles", 2: "A/P3 placed + J^T (+ CTA barrier)",
+         3: "(unused)", 4: "B totals + assemble + step", 8: "pick polish", 9: "re-eval + validate"}
 tot = out.sum()
 print(f"scene {scene_name}: {solves} solves, {outers} outers; cycles by phase (thread 0, summed over CTAs):")
 tot = out[:12].sum()

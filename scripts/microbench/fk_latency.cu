@@ -1,0 +1,95 @@
+// Microbenchmark: latency (cycles per call, one CTA) of the tile-cooperative FK (coop.cuh
+// tile_fk) and of one damped-least-squares polish iteration's pieces, with 1 warp and with
+// 6 warps resident (the C2 AL CTA shape). fp32, 7-DOF spatial chain with random axes.
+// Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 --expt-relaxed-constexpr
+//        -ftz=true -prec-div=false -prec-sqrt=false -I../../paper_2510_07674_b200/csrc -o fk_latency fk_latency.cu
+#include <cstdio>
+#include "coop.cuh"
+using namespace spasm;
+
+__global__ void k_fk(const ChainDesc<float>* g_ch, int iters, float* out, long long* cyc) {
+  __shared__ ChainDesc<float> ch;
+  if (threadIdx.x == 0) ch = *g_ch;
+  __syncthreads();
+  const Tile tl = Tile::make_warp();
+  LaneChain<float> lc;
+  lc.load(ch, tl.j);
+  float q = 0.1f * tl.j + 0.01f * (threadIdx.x >> 3);
+  TileFrame<float> f;
+  float acc = 0.f;
+  long long t0 = clock64();
+  for (int i = 0; i < iters; ++i) {
+    tile_fk(tl, lc, q, f);
+    q += f.ee[0] * 1e-3f;  // carry a dependency into the next call
+    acc += f.Ree[4];
+  }
+  long long t1 = clock64();
+  if (threadIdx.x == 0) cyc[blockIdx.x] = (t1 - t0) / iters;
+  out[threadIdx.x] = acc + q;
+}
+
+__global__ void k_dls(const ChainDesc<float>* g_ch, int iters, float* out, long long* cyc) {
+  __shared__ ChainDesc<float> ch;
+  if (threadIdx.x == 0) ch = *g_ch;
+  __syncthreads();
+  const Tile tl = Tile::make_warp();
+  float col[5], e[5];
+  for (int k = 0; k < 5; ++k) { col[k] = 0.1f * (k + 1) + 0.01f * tl.j; e[k] = 0.01f * k; }
+  float acc = 0.f;
+  long long t0 = clock64();
+  for (int i = 0; i < iters; ++i) {
+    const float dq = tile_dls<float, 5>(tl, col, e, 1e-3f);
+    col[0] += dq * 1e-3f;
+    acc += dq;
+  }
+  long long t1 = clock64();
+  if (threadIdx.x == 0) cyc[blockIdx.x] = (t1 - t0) / iters;
+  out[threadIdx.x] = acc;
+}
+
+__global__ void k_shfl(int iters, float* out, long long* cyc) {
+  float v = threadIdx.x;
+  long long t0 = clock64();
+  for (int i = 0; i < iters; ++i) v = __shfl_up_sync(0xffffffffu, v, 1, 8) + 1.f;
+  long long t1 = clock64();
+  if (threadIdx.x == 0) cyc[blockIdx.x] = (t1 - t0) / iters;
+  out[threadIdx.x] = v;
+}
+
+__global__ void k_lds(const float* g, int iters, float* out, long long* cyc) {
+  __shared__ float s[1024];
+  for (int i = threadIdx.x; i < 1024; i += blockDim.x) s[i] = (float)(i % 7);
+  __syncthreads();
+  int k = threadIdx.x & 7;
+  long long t0 = clock64();
+  for (int i = 0; i < iters; ++i) k = (int)s[k * 8 + (threadIdx.x & 7)];
+  long long t1 = clock64();
+  if (threadIdx.x == 0) cyc[blockIdx.x] = (t1 - t0) / iters;
+  out[threadIdx.x] = k;
+}
+
+int main() {
+  ChainDesc<float> h{};
+  h.J = 7;
+  for (int j = 0; j < 7; ++j) {
+    h.axis[j][0] = (j % 3 == 0); h.axis[j][1] = (j % 3 == 1); h.axis[j][2] = (j % 3 == 2);
+    h.offset[j][0] = 0.1f; h.offset[j][1] = 0.f; h.offset[j][2] = 0.2f;
+    h.lo[j] = -3.f; h.hi[j] = 3.f;
+  }
+  for (int c = 0; c < 9; ++c) h.tool_R[c] = (c % 4 == 0);
+  ChainDesc<float>* d; cudaMalloc(&d, sizeof(h)); cudaMemcpy(d, &h, sizeof(h), cudaMemcpyHostToDevice);
+  float* out; cudaMalloc(&out, 4096 * 4);
+  long long* cyc; cudaMalloc(&cyc, 64 * 8);
+  long long hc[1];
+  for (int threads : {32, 192}) {
+    k_fk<<<1, threads>>>(d, 1000, out, cyc); cudaMemcpy(hc, cyc, 8, cudaMemcpyDeviceToHost);
+    printf("tile_fk      %3d threads: %lld cycles/call\n", threads, hc[0]);
+    k_dls<<<1, threads>>>(d, 1000, out, cyc); cudaMemcpy(hc, cyc, 8, cudaMemcpyDeviceToHost);
+    printf("tile_dls<5>  %3d threads: %lld cycles/call\n", threads, hc[0]);
+    k_shfl<<<1, threads>>>(1000, out, cyc); cudaMemcpy(hc, cyc, 8, cudaMemcpyDeviceToHost);
+    printf("shfl+fadd    %3d threads: %lld cycles/iter\n", threads, hc[0]);
+    k_lds<<<1, threads>>>(nullptr, 1000, out, cyc); cudaMemcpy(hc, cyc, 8, cudaMemcpyDeviceToHost);
+    printf("lds chain    %3d threads: %lld cycles/iter\n", threads, hc[0]);
+  }
+  return 0;
+}
