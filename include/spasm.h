@@ -167,6 +167,20 @@ typedef struct {
   double device_ms;       /* stream time of the solve (CUDA events) */
 } spasm_solve_report;
 
+/* spasm_solve in two halves, for callers that chain device work after stage 1 without a
+ * host round trip (bench_api.solve_scene -> stage-2 lifting): spasm_solve_launch starts the
+ * solve (with a repeated shape the whole restart loop is ONE CUDA graph launch -- a
+ * conditional WHILE node, success test on the device -- and the call returns at once);
+ * spasm_solve_device_rows gives device pointers to the compacted result rows (float64,
+ * p_return x D) and their count (int32), valid in stream order after the launch;
+ * spasm_solve_collect waits (the one host sync) and fills the same outputs as spasm_solve.
+ * One pending solve per model. */
+int spasm_solve_launch(const spasm_model* model, int dtype, const spasm_solve_config* cfg, const double* warm_host,
+                       int64_t n_warm, void* workspace, int64_t workspace_bytes, void* stream);
+int spasm_solve_device_rows(const spasm_model* model, const double** rows, const int32_t** n_rows);
+int spasm_solve_collect(const spasm_model* model, double* particles, double* costs, int64_t* indices,
+                        spasm_solve_report* report);
+
 int64_t spasm_solve_workspace_bytes(const spasm_model* model, int dtype, const spasm_solve_config* cfg,
                                     int64_t n_warm);
 /* Runs the restart loop on `stream`. Outputs (host): particles[p_return*D], costs[p_return],
@@ -289,12 +303,14 @@ int spasm_traj_evaluate(const spasm_traj* traj, int dtype, const spasm_al_config
 /* validate (trajopt.py:1071-1153) for P trajectories. */
 int spasm_traj_validate(const spasm_traj* traj, int dtype, const spasm_al_config* cfg, const void* values,
                         int64_t P, uint8_t* feasible, void* violation, void* stream);
-/* lift_placements (trajopt.py:795-876), asynchronous: placements (P,D) float64 device rows.
- * Writes endpoints (kept,B,2,dof), kept[] row indices and status[2] = {first unreachable
- * staged pose or -1, kept count} on the device. */
+/* lift_placements (trajopt.py:795-876), asynchronous: placements (P,D) float64 device rows;
+ * n_rows (device int32, optional): only the first min(P, *n_rows) rows exist (the stage-1
+ * result read in place, spasm_solve_device_rows). Writes endpoints (kept,B,2,dof), kept[]
+ * row indices and status[2] = {first unreachable staged pose or -1, kept count} on the
+ * device. */
 int64_t spasm_lift_workspace_bytes(const spasm_traj* traj, int dtype, int64_t P, int candidates);
-int spasm_lift(const spasm_traj* traj, int dtype, const double* placements, int64_t P, int D, uint64_t seed,
-               int candidates, void* workspace, int64_t workspace_bytes, void* endpoints, int32_t* kept,
+int spasm_lift(const spasm_traj* traj, int dtype, const double* placements, int64_t P, const int32_t* n_rows, int D,
+               uint64_t seed, int candidates, void* workspace, int64_t workspace_bytes, void* endpoints, int32_t* kept,
                int32_t* status, void* stream);
 /* init_trajectories (trajopt.py:892-923) from a PCG64 state (the Generator the caller passes);
  * n_active (device, optional) bounds the live rows. spasm_trajectory_stream_state gives the

@@ -8,7 +8,7 @@ from __future__ import annotations
 
 import ctypes
 import os
-from ctypes import POINTER, c_char_p, c_double, c_int, c_int32, c_int64, c_uint8, c_uint32, c_uint64, c_void_p
+from ctypes import POINTER, byref, c_char_p, c_double, c_int, c_int32, c_int64, c_uint8, c_uint32, c_uint64, c_void_p
 
 import numpy as np
 
@@ -191,6 +191,10 @@ SIGNATURES = {
         [c_void_p, c_int, POINTER(spasm_solve_config), c_void_p, c_int64, c_void_p, c_int64, c_void_p, c_void_p,
          c_void_p, POINTER(spasm_solve_report), c_void_p, c_void_p, c_void_p, c_void_p],
     ),
+    "spasm_solve_launch": (
+        c_int, [c_void_p, c_int, POINTER(spasm_solve_config), c_void_p, c_int64, c_void_p, c_int64, c_void_p]),
+    "spasm_solve_collect": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, POINTER(spasm_solve_report)]),
+    "spasm_solve_device_rows": (c_int, [c_void_p, POINTER(c_void_p), POINTER(c_void_p)]),
     "spasm_shard_workspace_bytes": (c_int64, [c_void_p, c_int, POINTER(spasm_solve_config), c_int64, c_int64]),
     "spasm_shard_select": (
         c_int,
@@ -223,7 +227,7 @@ SIGNATURES = {
     "spasm_lift_workspace_bytes": (c_int64, [c_void_p, c_int, c_int64, c_int]),
     "spasm_lift": (
         c_int,
-        [c_void_p, c_int, c_void_p, c_int64, c_int, c_uint64, c_int, c_void_p, c_int64, c_void_p, c_void_p,
+        [c_void_p, c_int, c_void_p, c_int64, c_void_p, c_int, c_uint64, c_int, c_void_p, c_int64, c_void_p, c_void_p,
          c_void_p, c_void_p],
     ),
     "spasm_trajectory_stream_state": (c_int, [c_uint64, POINTER(c_uint64)]),

@@ -14,7 +14,7 @@ from typing import Optional
 
 import numpy as np
 
-from .particle_opt import OptimizerConfig, solve
+from .particle_opt import NativeCostModel, OptimizerConfig, solve, solve_launch
 from .problems import MotionProblem, Scene, as_cost_model
 
 STEP_CAP = 30000
@@ -78,16 +78,34 @@ def solve_scene(scene: Scene, *, seed: int = 0, threads: int = 1, solver_overrid
     config = replace(config, max_restarts=effective_max_restarts(config))
     run_stage2 = scene.chain is not None and not no_trajopt
     t0 = time.perf_counter()
+    pending = None
     if comm is not None and comm.world > 1:
         from .sharded import solve_sharded
 
         result = solve_sharded(model, config, comm=comm, warm_seeds=warm_seeds)
+    elif run_stage2 and isinstance(model, NativeCostModel) and config.reference_update:
+        # one host sync for the whole pipeline: stage 1 is launched (its restart loop is a
+        # device-side graph loop), stage 2 reads its rows in place and is enqueued behind it,
+        # and both are read back after the AL solve (trajopt.solve_stage2)
+        pending = solve_launch(model, config, warm_seeds=warm_seeds)
+        result = None
     else:
         result = solve(model, config, warm_seeds=warm_seeds, threads=threads)
+    if pending is not None:
+        from .trajopt import solve_stage2
+
+        sol, result = solve_stage2(scene, None, config, seed, trajopt_overrides, t0, precision=precision,
+                                   pending=pending)
+    stage1_ms = (time.perf_counter() - t0) * 1e3 if pending is None else None
     restarts_run = result.report.restarts + 1 if result.success else config.max_restarts
     stats = {"stage1_iterations": restarts_run * config.m * (config.k_lin + config.k_quad),
              "stage1_evaluations": restarts_run * config.n, "stage1_launches": result.report.launches,
-             "stage1_ms": (time.perf_counter() - t0) * 1e3}
+             "stage1_ms": stage1_ms if stage1_ms is not None else result.report.device_ms}
+    if pending is not None and sol is not None:
+        sol.stats = {**stats, **sol.stats}
+        sol.bookkeeping = {"restarts": int(result.report.restarts), "stage1_indices": np.asarray(result.indices).copy(),
+                           **sol.bookkeeping}
+        return sol
     if not result.success:
         return SceneSolution(False, (time.perf_counter() - t0) * 1e3, result.report.restarts, result.report.steps,
                              math.nan, stats=stats, bookkeeping={"restarts": int(result.report.restarts)})
@@ -101,7 +119,7 @@ def solve_scene(scene: Scene, *, seed: int = 0, threads: int = 1, solver_overrid
                                           "stage1_indices": np.asarray(result.indices).copy()})
     from .trajopt import solve_stage2
 
-    sol = solve_stage2(scene, result, config, seed, trajopt_overrides, t0, precision=precision)
+    sol, _ = solve_stage2(scene, result, config, seed, trajopt_overrides, t0, precision=precision)
     sol.stats = {**stats, **sol.stats}
     sol.bookkeeping = {"restarts": int(result.report.restarts), "stage1_indices": np.asarray(result.indices).copy(),
                        **sol.bookkeeping}

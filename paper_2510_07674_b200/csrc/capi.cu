@@ -5,6 +5,7 @@
 // sample+evaluate, the stable top-M sort, the fused descent schedule, the satisfying
 // ordering and the re-check, then reads back one small result block.
 #include <algorithm>
+#include <cuda_runtime.h>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -14,6 +15,7 @@
 #include "../../include/spasm.h"
 #include "model.hpp"
 #include "rng.cuh"
+#include "seedseq.cuh"
 #include "scene.cuh"
 #include "launchers.hpp"
 
@@ -117,6 +119,9 @@ __global__ void k_trace_ids(const uint32_t* __restrict__ top, int n, int32_t* __
 }
 
 // ---- workspace layout -------------------------------------------------------------
+struct ResLayout;
+static size_t res_layout_bytes(int D, int p);
+
 struct SolveLayout {
   size_t values, keys0, keys1, idx0, idx1, hist, opt_values, opt_cost, flagged, counters, skeys0, skeys1, svals0,
       svals1, chosen_vals, recheck, warm, res, total;
@@ -159,8 +164,8 @@ static SolveLayout make_layout(int D, const spasm_solve_config& cfg, int64_t n_w
   L.chosen_vals = take((size_t)cfg.p_return * D * sizeof(R));
   L.recheck = take((size_t)cfg.p_return * sizeof(R));
   L.warm = take((size_t)std::max<int64_t>(n_warm, 1) * D * 8);
-  // result block: counters(64B) | out_vals p*D doubles | out_cost p doubles | recheck p doubles | idx p int32
-  L.res_bytes = 64 + (size_t)cfg.p_return * D * 8 + (size_t)cfg.p_return * 8 * 2 + (size_t)cfg.p_return * 4;
+  // result block (res_layout): counters | out_* (last restart) | final_* (compacted)
+  L.res_bytes = res_layout_bytes(D, cfg.p_return);
   L.res = take(L.res_bytes);
   L.total = off;
   return L;
@@ -197,15 +202,121 @@ StepRule step_rule(const spasm_solve_config& cfg, int restart) {
   return r;
 }
 
+// ---- the restart loop on the device (CUDA graph with a conditional WHILE node) ------------
+// The result block in the workspace (copied to pinned host memory once, at the end):
+//   counters  [0] n_sat  [1] flagged (both reset per restart)
+//             [8] last restart run  [9] stopped  [10] flagged total  [11] n_final  [12] success
+//   out_*     the last restart's first p_return satisfying rows (stable cost order), their
+//             costs, re-check costs and batch indices (k_gather_chosen / k_copy_recheck)
+//   final_*   the rows that passed the re-check, compacted (particle_opt.py:366 chosen =
+//             chosen[satisfaction]); device consumers (stage-2 lifting) read these in place
+struct ResLayout {
+  size_t vals, cost, recheck, idx, fvals, fcost, fidx, bytes;
+};
+static ResLayout res_layout(int D, int p) {
+  ResLayout r;
+  size_t o = 64;
+  r.vals = o;
+  o += (size_t)p * D * 8;
+  r.cost = o;
+  o += (size_t)p * 8;
+  r.recheck = o;
+  o += (size_t)p * 8;
+  r.idx = o;
+  o += (size_t)p * 4;
+  o = (o + 7) & ~(size_t)7;
+  r.fvals = o;
+  o += (size_t)p * D * 8;
+  r.fcost = o;
+  o += (size_t)p * 8;
+  r.fidx = o;
+  o += (size_t)p * 4;
+  r.bytes = (o + 63) & ~(size_t)63;
+  return r;
+}
+
+static size_t res_layout_bytes(int D, int p) { return res_layout(D, p).bytes; }
+
+// chosen = chosen[recheck < eps], compacted (one thread; p_return is small)
+__device__ void compact_chosen(char* res, const ResLayout RL, int p, int D, double eps) {
+  unsigned int* c = reinterpret_cast<unsigned int*>(res);
+  const int k = min((int)c[0], p);
+  const double* v = reinterpret_cast<const double*>(res + RL.vals);
+  const double* co = reinterpret_cast<const double*>(res + RL.cost);
+  const double* re = reinterpret_cast<const double*>(res + RL.recheck);
+  const int32_t* ix = reinterpret_cast<const int32_t*>(res + RL.idx);
+  double* fv = reinterpret_cast<double*>(res + RL.fvals);
+  double* fc = reinterpret_cast<double*>(res + RL.fcost);
+  int32_t* fi = reinterpret_cast<int32_t*>(res + RL.fidx);
+  int w = 0;
+  for (int i = 0; i < k; ++i) {
+    if (!(re[i] < eps)) continue;
+    for (int d = 0; d < D; ++d) fv[(int64_t)w * D + d] = v[(int64_t)i * D + d];
+    fc[w] = co[i];
+    fi[w] = ix[i];
+    ++w;
+  }
+  c[11] = (unsigned)w;
+  c[12] = w > 0 ? 1u : 0u;
+}
+
+__global__ void k_finalize(char* res, ResLayout RL, int p, int D, double eps) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) compact_chosen(res, RL, p, D, eps);
+}
+
+// restart r's PCG64 state = SeedSequence(entropy=seed, spawn_key=(r,)) (particle_opt.py:176-178)
+__global__ void k_restart_begin(RestartParams* rp) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) rp->st = seedseq_pcg64_dev(rp->seed, rp->restart);
+}
+
+// end of one restart: accumulate the flag count; stop at the first restart with any
+// satisfying particle (particle_opt.py:360-376) or after max_restarts (:325, :385-400)
+__global__ void k_restart_end(cudaGraphConditionalHandle h, RestartParams* rp, char* res, ResLayout RL, int p, int D,
+                              double eps, int max_restarts) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  unsigned int* c = reinterpret_cast<unsigned int*>(res);
+  c[10] += c[1];
+  const unsigned int r = rp->restart;
+  c[8] = r;
+  const bool sat = c[0] > 0;
+  const bool stop = sat || (int)r + 1 >= max_restarts;
+  if (sat) compact_chosen(res, RL, p, D, eps);
+  c[9] = stop ? 1u : 0u;
+  if (!stop) rp->restart = r + 1;
+  cudaGraphSetConditional(h, stop ? 0u : 1u);
+}
+
+// the timing events of a pending solve
+struct EventPair {
+  cudaEvent_t a = nullptr, b = nullptr;
+  ~EventPair() {
+    if (a) cudaEventDestroy(a);
+    if (b) cudaEventDestroy(b);
+  }
+};
+
 template <typename R>
-static int solve_impl(Model& m, const spasm_solve_config& cfg, const double* warm_host, int64_t n_warm, void* ws,
-                      int64_t ws_bytes, double* particles, double* costs, int64_t* indices, spasm_solve_report* rep,
-                      R* trace_cost, uint8_t* trace_sat, int32_t* trace_ids, cudaStream_t s) {
+static int restart_launch_count(const Model& m, const spasm_solve_config& cfg, bool tr) {
+  // sample_eval [+ tile keys], 2 sorts (3 kernels per 8-bit pass), schedule, [trace ids],
+  // sat keys, gather, re-check evaluate, re-check copy
+  const int bits = 8 * (int)sizeof(R);
+  const int sample = (sizeof(R) == 4 && m.tile_ok && stage1_tile_mode() != 0) ? 2 : 1;
+  return sample + radix_sort_launches(cfg.n, bits) + 1 + (tr ? 1 : 0) + 1 + radix_sort_launches(cfg.m, bits) + 3;
+}
+
+// Starts a solve. Graph path (reference step rule, no trace, a repeated shape): ONE graph
+// launch runs every restart on the device -- no host round trip until solve_collect.
+// Otherwise the restarts run from the host (one sync per restart) and the result is parsed
+// here. Either way solve_collect returns it.
+template <typename R>
+static int solve_launch(Model& m, const spasm_solve_config& cfg, const double* warm_host, int64_t n_warm, void* ws,
+                        int64_t ws_bytes, R* trace_cost, uint8_t* trace_sat, int32_t* trace_ids, cudaStream_t s) {
   using K = typename KeyOf<R>::type;
   const int D = m.dim;
   SolveLayout L = make_layout<R>(D, cfg, n_warm);
   SPASM_REQUIRE(ws != nullptr && (size_t)ws_bytes >= L.total, "solve workspace too small");
   SPASM_REQUIRE(n_warm >= 0 && n_warm <= cfg.n, "more warm seeds than particles");
+  const ResLayout RL = res_layout(D, cfg.p_return);
   char* base = static_cast<char*>(ws);
   R* values = reinterpret_cast<R*>(base + L.values);
   K* keys0 = reinterpret_cast<K*>(base + L.keys0);
@@ -224,11 +335,11 @@ static int solve_impl(Model& m, const spasm_solve_config& cfg, const double* war
   R* recheck = reinterpret_cast<R*>(base + L.recheck);
   double* warm_dev = reinterpret_cast<double*>(base + L.warm);
   char* res = base + L.res;
-  unsigned int* counters = reinterpret_cast<unsigned int*>(res);  // [0]=n_sat [1]=flagged
-  double* out_vals = reinterpret_cast<double*>(res + 64);
-  double* out_cost = out_vals + (size_t)cfg.p_return * D;
-  double* out_recheck = out_cost + cfg.p_return;
-  int32_t* out_idx = reinterpret_cast<int32_t*>(out_recheck + cfg.p_return);
+  unsigned int* counters = reinterpret_cast<unsigned int*>(res);
+  double* out_vals = reinterpret_cast<double*>(res + RL.vals);
+  double* out_cost = reinterpret_cast<double*>(res + RL.cost);
+  double* out_recheck = reinterpret_cast<double*>(res + RL.recheck);
+  int32_t* out_idx = reinterpret_cast<int32_t*>(res + RL.idx);
 
   if (m.pinned_bytes < L.res_bytes) {
     pinned_put(m.pinned, m.pinned_bytes);
@@ -237,30 +348,25 @@ static int solve_impl(Model& m, const spasm_solve_config& cfg, const double* war
     SPASM_CUDA_TRY(pinned_get(&m.pinned, L.res_bytes, &m.pinned_bytes));
   }
   char* host = static_cast<char*>(m.pinned);
+  SolvePending& P = m.pend;
+  P = SolvePending{};
+  P.dtype_size = (int)sizeof(R);
+  P.cfg = cfg;
+  P.res_bytes = L.res_bytes;
+  P.res_dev = res;
+  P.ws = ws;
+  P.n_warm = n_warm;
 
   if (n_warm > 0)
     SPASM_CUDA_TRY(cudaMemcpyAsync(warm_dev, warm_host, (size_t)n_warm * D * 8, cudaMemcpyHostToDevice, s));
+  if (!m.ev0) SPASM_CUDA_TRY(cudaEventCreate(&m.ev0));
+  if (!m.ev1) SPASM_CUDA_TRY(cudaEventCreate(&m.ev1));
+  SPASM_CUDA_TRY(cudaEventRecord(m.ev0, s));
 
-  // the timing events are destroyed on every return path (early errors included)
-  struct EventPair {
-    cudaEvent_t a = nullptr, b = nullptr;
-    ~EventPair() {
-      if (a) cudaEventDestroy(a);
-      if (b) cudaEventDestroy(b);
-    }
-  } ev;
-  SPASM_CUDA_TRY(cudaEventCreate(&ev.a));
-  SPASM_CUDA_TRY(cudaEventCreate(&ev.b));
-  cudaEvent_t e0 = ev.a, e1 = ev.b;
-  SPASM_CUDA_TRY(cudaEventRecord(e0, s));
-
-  int total_steps = 0, total_flagged = 0, launches = 0;
-  const int per_restart = cfg.k_lin + cfg.k_quad;
-  int rc = SPASM_NO_SOLUTION;
-  std::memset(rep, 0, sizeof(*rep));
   const bool tr = trace_cost != nullptr && cfg.n_traced > 0;
+  const int per_restart_launches = restart_launch_count<R>(m, cfg, tr && trace_ids);
 
-  // One restart's device work on stream ss, ending with the D2H copy of the result block.
+  // One restart's device work on stream ss (no host copy: the result block stays on the device).
   auto body = [&](int restart, const Pcg64State& st, cudaStream_t ss) -> int {
     int r = launch_sample_eval<R>(m, st, 0, cfg.n, n_warm ? warm_dev : nullptr, n_warm, cfg.sampler, cfg.seed,
                                   (uint32_t)restart, values, keys0, idx0, ss);
@@ -268,7 +374,7 @@ static int solve_impl(Model& m, const spasm_solve_config& cfg, const double* war
     bool in1 = false;
     if ((r = launch_sort<R>(keys0, idx0, keys1, idx1, cfg.n, hist, &in1, ss))) return r;
     const uint32_t* top = in1 ? idx1 : idx0;
-    SPASM_CUDA_TRY(cudaMemsetAsync(res, 0, 64, ss));
+    SPASM_CUDA_TRY(cudaMemsetAsync(res, 0, 16, ss));  // per-restart counters; the loop state persists
     if ((r = launch_schedule<R>(m, values, top, cfg.m, cfg.k_lin, cfg.k_quad, cfg.eta_init, cfg.alpha, cfg.epsilon,
                                 opt_values, opt_cost, flagged, counters + 1, tr ? trace_cost : nullptr,
                                 tr ? trace_sat : nullptr, tr ? cfg.n_traced : 0, step_rule(cfg, restart), ss)))
@@ -288,14 +394,13 @@ static int solve_impl(Model& m, const spasm_solve_config& cfg, const double* war
     if ((r = launch_evaluate<R>(m, chosen_vals, cfg.p_return, 1, recheck, ss))) return r;
     k_copy_recheck<R><<<ceil_div(cfg.p_return, 128), 128, 0, ss>>>(recheck, cfg.p_return, out_recheck);
     SPASM_CHECK_LAUNCH();
-    SPASM_CUDA_TRY(cudaMemcpyAsync(host, res, L.res_bytes, cudaMemcpyDeviceToHost, ss));
     return SPASM_OK;
   };
 
-  // CUDA graph of the restart (reference GD step, no trace): captured once per (model,
-  // workspace, config) and relaunched for every restart and every later solve with the
-  // same shapes; the restart's PCG64 state / seed / index travel through device memory
-  // (RestartParams), refreshed by the graph's first node from pinned host memory.
+  // graph of the whole restart loop (reference GD step, no trace): built once per (model,
+  // workspace, config) and relaunched for every later solve with the same shapes:
+  //   memset(loop state) -> H2D(seed) -> WHILE { k_restart_begin, restart body, k_restart_end }
+  //   -> D2H(result block)
   bool use_graph = g_graphs && !tr && step_rule(cfg, 0).is_reference();
   if (use_graph) {
     Model::GraphKeyPod key;
@@ -311,6 +416,7 @@ static int solve_impl(Model& m, const spasm_solve_config& cfg, const double* war
     key.alpha = cfg.alpha;
     key.eps = cfg.epsilon;
     key.p_return = cfg.p_return;
+    key.max_restarts = cfg.max_restarts;
     key.sampler = cfg.sampler;
     key.n_warm = n_warm;
     key.tile = stage1_tile_mode();
@@ -329,81 +435,163 @@ static int solve_impl(Model& m, const spasm_solve_config& cfg, const double* war
       if (!m.cap) SPASM_CUDA_TRY(cudaStreamCreateWithFlags(&m.cap, cudaStreamNonBlocking));
       if (!m.rp_dev) SPASM_CUDA_TRY(cudaMalloc(&m.rp_dev, sizeof(RestartParams)));
       if (!m.rp_host) SPASM_CUDA_TRY(cudaMallocHost(&m.rp_host, sizeof(RestartParams)));
-      SPASM_CUDA_TRY(cudaStreamBeginCapture(m.cap, cudaStreamCaptureModeThreadLocal));
-      cudaMemcpyAsync(m.rp_dev, m.rp_host, sizeof(RestartParams), cudaMemcpyHostToDevice, m.cap);
+      cudaGraph_t g = nullptr;
+      SPASM_CUDA_TRY(cudaGraphCreate(&g, 0));
+      struct GraphGuard {
+        cudaGraph_t g;
+        ~GraphGuard() {
+          if (g) cudaGraphDestroy(g);
+        }
+      } guard{g};
+      cudaGraphConditionalHandle h;
+      SPASM_CUDA_TRY(cudaGraphConditionalHandleCreate(&h, g, 1, cudaGraphCondAssignDefault));
+      cudaGraphNode_t n_set, n_rp, n_loop, n_out;
+      cudaMemsetParams ms{};
+      ms.dst = res;
+      ms.value = 0;
+      ms.elementSize = 4;
+      ms.width = 16;  // the 64-byte counter block
+      ms.height = 1;
+      SPASM_CUDA_TRY(cudaGraphAddMemsetNode(&n_set, g, nullptr, 0, &ms));
+      SPASM_CUDA_TRY(cudaGraphAddMemcpyNode1D(&n_rp, g, &n_set, 1, m.rp_dev, m.rp_host, sizeof(RestartParams),
+                                              cudaMemcpyHostToDevice));
+      cudaGraphNodeParams wp{};
+      wp.type = cudaGraphNodeTypeConditional;
+      wp.conditional.handle = h;
+      wp.conditional.type = cudaGraphCondTypeWhile;
+      wp.conditional.size = 1;
+      SPASM_CUDA_TRY(cudaGraphAddNode(&n_loop, g, &n_rp, 1, &wp));
+      cudaGraph_t loop_body = wp.conditional.phGraph_out[0];
+      SPASM_CUDA_TRY(cudaStreamBeginCaptureToGraph(m.cap, loop_body, nullptr, nullptr, 0,
+                                                   cudaStreamCaptureModeThreadLocal));
+      k_restart_begin<<<1, 1, 0, m.cap>>>(m.rp_dev);
       g_restart_override = m.rp_dev;
-      const int r = body(0, restart_state(cfg.seed, 0), m.cap);
+      int r = body(0, restart_state(cfg.seed, 0), m.cap);
       g_restart_override = nullptr;
-      cudaGraph_t graph = nullptr;
-      const cudaError_t ec = cudaStreamEndCapture(m.cap, &graph);
-      if (r || ec != cudaSuccess) {
-        if (graph) cudaGraphDestroy(graph);
-        if (r) return r;
-        SPASM_CUDA_TRY(ec);
+      if (!r) {
+        k_restart_end<<<1, 32, 0, m.cap>>>(h, m.rp_dev, res, RL, cfg.p_return, D, cfg.epsilon, cfg.max_restarts);
+        if (cudaGetLastError() != cudaSuccess) r = SPASM_ERR_CUDA;
       }
-      const cudaError_t ei = cudaGraphInstantiate(&m.gexec, graph, 0);
-      cudaGraphDestroy(graph);
-      SPASM_CUDA_TRY(ei);
+      cudaGraph_t captured = nullptr;
+      const cudaError_t ec = cudaStreamEndCapture(m.cap, &captured);
+      if (r) {
+        if (r == SPASM_ERR_CUDA) set_last_error("restart-loop capture: kernel launch failed");
+        return r;
+      }
+      SPASM_CUDA_TRY(ec);
+      SPASM_CUDA_TRY(cudaGraphAddMemcpyNode1D(&n_out, g, &n_loop, 1, host, res, L.res_bytes, cudaMemcpyDeviceToHost));
+      SPASM_CUDA_TRY(cudaGraphInstantiate(&m.gexec, g, 0));
       m.gkey = key;
     }
+    m.rp_host->seed = cfg.seed;
+    m.rp_host->restart = 0;
+    SPASM_CUDA_TRY(cudaGraphLaunch(m.gexec, s));
+    SPASM_CUDA_TRY(cudaEventRecord(m.ev1, s));
+    P.graph = true;
+    P.per_restart_launches = per_restart_launches + 2;  // + k_restart_begin / k_restart_end
+    P.active = true;
+    return SPASM_OK;
   }
 
+  // host-driven restarts: one sync per restart to read n_sat (particle_opt.py:325-376)
+  SPASM_CUDA_TRY(cudaMemsetAsync(res, 0, 64, s));
+  const int per_restart = cfg.k_lin + cfg.k_quad;
+  const double* h_vals = reinterpret_cast<const double*>(host + RL.vals);
+  const double* h_cost = reinterpret_cast<const double*>(host + RL.cost);
+  const double* h_re = reinterpret_cast<const double*>(host + RL.recheck);
+  const int32_t* h_idx = reinterpret_cast<const int32_t*>(host + RL.idx);
+  spasm_solve_report& rep = P.rep;
+  std::memset(&rep, 0, sizeof(rep));
+  P.rc = SPASM_NO_SOLUTION;
+  P.rows.clear();
+  int total_steps = 0, total_flagged = 0, launches = 0;
   for (int restart = 0; restart < cfg.max_restarts; ++restart) {
-    const Pcg64State st = restart_state(cfg.seed, (uint64_t)restart);
-    if (use_graph) {
-      m.rp_host->st = st;
-      m.rp_host->seed = cfg.seed;
-      m.rp_host->restart = (uint32_t)restart;
-      SPASM_CUDA_TRY(cudaGraphLaunch(m.gexec, s));
-    } else {
-      const int r = body(restart, st, s);
-      if (r) return r;
-    }
+    const int r = body(restart, restart_state(cfg.seed, (uint64_t)restart), s);
+    if (r) return r;
+    SPASM_CUDA_TRY(cudaMemcpyAsync(host, res, L.res_bytes, cudaMemcpyDeviceToHost, s));
     SPASM_CUDA_TRY(cudaStreamSynchronize(s));
-
     const unsigned int* hc = reinterpret_cast<const unsigned int*>(host);
-    const double* h_vals = reinterpret_cast<const double*>(host + 64);
-    const double* h_cost = h_vals + (size_t)cfg.p_return * D;
-    const double* h_re = h_cost + cfg.p_return;
-    const int32_t* h_idx = reinterpret_cast<const int32_t*>(h_re + cfg.p_return);
     total_steps += per_restart;
-    {  // kernels this restart launched: sample_eval, 2 sorts (3 kernels per 8-bit pass),
-       // schedule, [trace ids], sat keys, gather, re-check evaluate, re-check copy
-      const int bits = 8 * (int)sizeof(R);
-      const int sample = (sizeof(R) == 4 && m.tile_ok && stage1_tile_mode() != 0) ? 2 : 1;  // k_sample + k_keys_tile
-      launches += sample + radix_sort_launches(cfg.n, bits) + 1 + (tr && trace_ids ? 1 : 0) + 1 +
-                  radix_sort_launches(cfg.m, bits) + 3;
-    }
+    launches += per_restart_launches;
     total_flagged += (int)hc[1];
     const int n_sat = (int)hc[0];
     if (n_sat > 0) {
       const int k = std::min(n_sat, (int)cfg.p_return);
-      int w = 0;
       for (int c = 0; c < k; ++c) {
         if (!(h_re[c] < cfg.epsilon)) continue;  // chosen = chosen[recheck]
-        std::memcpy(particles + (size_t)w * D, h_vals + (size_t)c * D, (size_t)D * 8);
-        costs[w] = h_cost[c];
-        indices[w] = h_idx[c];
-        ++w;
+        P.rows.insert(P.rows.end(), h_vals + (size_t)c * D, h_vals + (size_t)(c + 1) * D);
+        P.costs.push_back(h_cost[c]);
+        P.idx.push_back(h_idx[c]);
       }
-      rep->success = w > 0;
-      rep->restarts = restart;
-      rep->n_satisfying = n_sat;
-      rep->n_chosen = w;
-      rc = w > 0 ? SPASM_OK : SPASM_NO_SOLUTION;
+      const int w = (int)P.costs.size();
+      rep.success = w > 0;
+      rep.restarts = restart;
+      rep.n_satisfying = n_sat;
+      rep.n_chosen = w;
+      P.rc = w > 0 ? SPASM_OK : SPASM_NO_SOLUTION;
+      // the compacted rows for device consumers (stage-2 lifting), as the graph path leaves them
+      k_finalize<<<1, 1, 0, s>>>(res, RL, cfg.p_return, D, cfg.epsilon);
+      SPASM_CHECK_LAUNCH();
+      launches += 1;
       break;
     }
-    rep->restarts = cfg.max_restarts;
+    rep.restarts = cfg.max_restarts;
   }
-  rep->steps = total_steps;
-  rep->launches = launches;
-  rep->flagged = total_flagged;
-  SPASM_CUDA_TRY(cudaEventRecord(e1, s));
-  SPASM_CUDA_TRY(cudaEventSynchronize(e1));
+  rep.steps = total_steps;
+  rep.launches = launches;
+  rep.flagged = total_flagged;
+  SPASM_CUDA_TRY(cudaEventRecord(m.ev1, s));
+  P.graph = false;
+  P.active = true;
+  return SPASM_OK;
+}
+
+// Waits for a launched solve (the only host sync of the graph path) and fills the outputs.
+static int solve_collect(Model& m, double* particles, double* costs, int64_t* indices, spasm_solve_report* rep) {
+  SolvePending& P = m.pend;
+  SPASM_REQUIRE(P.active, "no launched solve to collect");
+  P.active = false;
+  const int D = m.dim;
+  const spasm_solve_config& cfg = P.cfg;
+  SPASM_CUDA_TRY(cudaEventSynchronize(m.ev1));
   float ms = 0.f;
-  cudaEventElapsedTime(&ms, e0, e1);
+  cudaEventElapsedTime(&ms, m.ev0, m.ev1);
+  if (!P.graph) {
+    *rep = P.rep;
+    rep->device_ms = ms;
+    const int w = (int)P.costs.size();
+    if (w > 0) std::memcpy(particles, P.rows.data(), (size_t)w * D * 8);
+    for (int c = 0; c < w; ++c) {
+      costs[c] = P.costs[c];
+      indices[c] = P.idx[c];
+    }
+    return P.rc;
+  }
+  const ResLayout RL = res_layout(D, cfg.p_return);
+  const char* host = static_cast<const char*>(m.pinned);
+  const unsigned int* hc = reinterpret_cast<const unsigned int*>(host);
+  std::memset(rep, 0, sizeof(*rep));
+  const int last = (int)hc[8];
+  const int n_sat = (int)hc[0];
+  const int runs = n_sat > 0 ? last + 1 : cfg.max_restarts;
+  rep->steps = runs * (cfg.k_lin + cfg.k_quad);
+  rep->launches = runs * P.per_restart_launches;
+  rep->flagged = (int)hc[10];
   rep->device_ms = ms;
-  return rc;
+  if (n_sat == 0) {
+    rep->restarts = cfg.max_restarts;
+    return SPASM_NO_SOLUTION;
+  }
+  const int w = (int)hc[11];
+  std::memcpy(particles, host + RL.fvals, (size_t)w * D * 8);
+  std::memcpy(costs, host + RL.fcost, (size_t)w * 8);
+  const int32_t* fi = reinterpret_cast<const int32_t*>(host + RL.fidx);
+  for (int c = 0; c < w; ++c) indices[c] = fi[c];
+  rep->success = w > 0;
+  rep->restarts = last;
+  rep->n_satisfying = n_sat;
+  rep->n_chosen = w;
+  return w > 0 ? SPASM_OK : SPASM_NO_SOLUTION;
 }
 
 }  // namespace spasm
@@ -713,6 +901,8 @@ void spasm_model_destroy(spasm_model* model) {
   if (model->cap) cudaStreamDestroy(model->cap);
   if (model->rp_dev) cudaFree(model->rp_dev);
   if (model->rp_host) cudaFreeHost(model->rp_host);
+  if (model->ev0) cudaEventDestroy(model->ev0);
+  if (model->ev1) cudaEventDestroy(model->ev1);
   delete model;
 }
 
@@ -844,9 +1034,37 @@ int spasm_solve(const spasm_model* model, int dtype, const spasm_solve_config* c
   if (r) return r;
   SPASM_REQUIRE(particles && costs && indices && report, "null output buffer");
   Model& m = const_cast<spasm_model&>(*model);
-  SPASM_DTYPE_SWITCH(dtype, return solve_impl<R>(m, *cfg, warm_host, n_warm, workspace, workspace_bytes, particles,
-                                                 costs, indices, report, static_cast<R*>(trace_cost), trace_sat,
-                                                 trace_ids, as_stream(stream)););
+  SPASM_DTYPE_SWITCH(dtype, r = solve_launch<R>(m, *cfg, warm_host, n_warm, workspace, workspace_bytes,
+                                                static_cast<R*>(trace_cost), trace_sat, trace_ids, as_stream(stream)););
+  if (r) return r;
+  return solve_collect(m, particles, costs, indices, report);
+}
+
+int spasm_solve_launch(const spasm_model* model, int dtype, const spasm_solve_config* cfg, const double* warm_host,
+                       int64_t n_warm, void* workspace, int64_t workspace_bytes, void* stream) {
+  SPASM_REQUIRE(model != nullptr, "null model");
+  int r = validate_cfg(cfg);
+  if (r) return r;
+  Model& m = const_cast<spasm_model&>(*model);
+  SPASM_DTYPE_SWITCH(dtype, return solve_launch<R>(m, *cfg, warm_host, n_warm, workspace, workspace_bytes, nullptr,
+                                                   nullptr, nullptr, as_stream(stream)););
+}
+
+int spasm_solve_collect(const spasm_model* model, double* particles, double* costs, int64_t* indices,
+                        spasm_solve_report* report) {
+  SPASM_REQUIRE(model != nullptr, "null model");
+  SPASM_REQUIRE(particles && costs && indices && report, "null output buffer");
+  return solve_collect(const_cast<spasm_model&>(*model), particles, costs, indices, report);
+}
+
+int spasm_solve_device_rows(const spasm_model* model, const double** rows, const int32_t** n_rows) {
+  SPASM_REQUIRE(model != nullptr && rows && n_rows, "null argument");
+  const Model& m = *model;
+  SPASM_REQUIRE(m.pend.res_dev != nullptr, "no launched solve");
+  const ResLayout RL = res_layout(m.dim, m.pend.cfg.p_return);
+  *rows = reinterpret_cast<const double*>(m.pend.res_dev + RL.fvals);
+  *n_rows = reinterpret_cast<const int32_t*>(m.pend.res_dev) + 11;
+  return SPASM_OK;
 }
 
 }  // extern "C"

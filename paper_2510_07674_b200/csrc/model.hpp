@@ -1,5 +1,8 @@
 // Host-side model object behind the opaque spasm_model handle.
 #pragma once
+#include <vector>
+
+#include "../../include/spasm.h"
 #include "scene.cuh"
 #include "rng.cuh"
 
@@ -13,6 +16,20 @@ void pinned_trim();
 
 
 enum class ModelKind { Tetris = 1, Tower = 2 };
+
+// a launched, not yet collected stage-1 solve (capi.cu solve_launch / solve_collect)
+struct SolvePending {
+  bool active = false, graph = false;
+  int dtype_size = 0, per_restart_launches = 0, rc = 0;
+  spasm_solve_config cfg{};
+  size_t res_bytes = 0;
+  char* res_dev = nullptr;
+  void* ws = nullptr;
+  int64_t n_warm = 0;
+  spasm_solve_report rep{};              // host-loop path: parsed result
+  std::vector<double> rows, costs;
+  std::vector<int64_t> idx;
+};
 
 struct Model {
   ModelKind kind;
@@ -43,10 +60,13 @@ struct Model {
     int64_t n, m;
     int k_lin, k_quad;
     double eta, alpha, eps;
-    int p_return, sampler;
+    int p_return, max_restarts, sampler;
     int64_t n_warm;
     int tile;
   } gkey{}, gkey_seen{};
+  // the solve launched by spasm_solve_launch, until spasm_solve_collect (capi.cu)
+  SolvePending pend;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
 
   template <typename R> const TetrisScene<R>& tetris() const;
   template <typename R> const TowerScene<R>& tower() const;

@@ -364,9 +364,9 @@ int spasm_ik_solve(const spasm_traj* t, int dtype, const double* target_pos, con
   out.pen = nullptr;
   if (dtype == SPASM_F32)
     return launch_ik<float>(*t, (int)n_targets, 1, seed, 0, restarts, max_iters, damping, target_pos, target_yaw,
-                            nullptr, 0, 0, 0, out, as_stream2(stream));
+                            nullptr, 0, 0, 0, out, as_stream2(stream), nullptr);
   return launch_ik<double>(*t, (int)n_targets, 1, seed, 0, restarts, max_iters, damping, target_pos, target_yaw,
-                           nullptr, 0, 0, 0, out, as_stream2(stream));
+                           nullptr, 0, 0, 0, out, as_stream2(stream), nullptr);
 }
 
 int spasm_polish_tool_down(const spasm_traj* t, int dtype, void* Q, const double* target_pos,
@@ -414,9 +414,9 @@ int64_t spasm_lift_workspace_bytes(const spasm_traj* t, int dtype, int64_t P, in
   return (int64_t)lift_ws_layout(*t, dtype, P, candidates).total;
 }
 
-int spasm_lift(const spasm_traj* t, int dtype, const double* placements, int64_t P, int D, uint64_t seed,
-               int candidates, void* ws, int64_t ws_bytes, void* endpoints, int32_t* kept, int32_t* status,
-               void* stream) {
+int spasm_lift(const spasm_traj* t, int dtype, const double* placements, int64_t P, const int32_t* n_rows, int D,
+               uint64_t seed, int candidates, void* ws, int64_t ws_bytes, void* endpoints, int32_t* kept,
+               int32_t* status, void* stream) {
   SPASM_TRAJ_GUARD(t);
   SPASM_DTYPE_GUARD(dtype);
   SPASM_REQUIRE(t->manip, "point-to-point problems carry their own endpoints");
@@ -440,18 +440,18 @@ int spasm_lift(const spasm_traj* t, int dtype, const double* placements, int64_t
   int st;
   if (dtype == SPASM_F32) {
     st = launch_ik<float>(*t, nt, cand, seed, 1000003ull, kIkRestarts, 200, kIkDamping, nullptr, nullptr, placements,
-                          D, 1, score, out, s);
+                          D, 1, score, out, s, n_rows);
     if (st) return st;
     return launch_lift_combine<float>((const float*)out.sol, out.ik_ok, out.pol_ok, (const float*)out.pen, nt, cand,
                                       t->J, t->B, (int)P, (float*)(b + L.best), (uint8_t*)(b + L.okt), kept,
-                                      (float*)endpoints, status, s);
+                                      (float*)endpoints, status, s, n_rows);
   }
   st = launch_ik<double>(*t, nt, cand, seed, 1000003ull, kIkRestarts, 200, kIkDamping, nullptr, nullptr, placements,
-                         D, 1, score, out, s);
+                         D, 1, score, out, s, n_rows);
   if (st) return st;
   return launch_lift_combine<double>((const double*)out.sol, out.ik_ok, out.pol_ok, (const double*)out.pen, nt, cand,
                                      t->J, t->B, (int)P, (double*)(b + L.best), (uint8_t*)(b + L.okt), kept,
-                                     (double*)endpoints, status, s);
+                                     (double*)endpoints, status, s, n_rows);
 }
 
 int spasm_trajectory_stream_state(uint64_t seed, uint64_t out[4]) {

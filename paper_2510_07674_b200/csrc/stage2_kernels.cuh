@@ -76,7 +76,10 @@ __global__ void __launch_bounds__(MAXT) k_ik_group(const TrajScene<R>* __restric
                                                   uint64_t seed, uint64_t draw_stride, int restarts, int max_iters,
                                                   double damping, const double* __restrict__ tpos_in,
                                                   const double* __restrict__ tyaw_in, const double* __restrict__ rows,
-                                                  int D, int polish, int score_statics, IkOut out) {
+                                                  int D, int polish, int score_statics, IkOut out,
+                                                  const int32_t* __restrict__ n_rows) {
+  // device row count (stage-1 result read in place): groups of absent rows exit at once
+  if (n_rows && (int)(blockIdx.x % n_targets) >= g_scene->B + *n_rows * g_scene->B) return;
   __shared__ ChainDesc<R> ch_s;
   __shared__ R s_key[32], s_score[32];
   __shared__ int s_ok[32];
@@ -202,11 +205,17 @@ __global__ void k_polish(const TrajScene<R>* __restrict__ g_scene, int n, R* __r
 template <typename R>
 __global__ void __launch_bounds__(1024) k_lift_combine(const R* __restrict__ sol, const uint8_t* __restrict__ ik_ok,
                                                        const uint8_t* __restrict__ pol_ok, const R* __restrict__ pen,
-                                                       int n_targets, int n_draws, int J, int B, int P,
+                                                       int stride_targets, int n_draws, int J, int B, int P,
                                                        R* __restrict__ best, uint8_t* __restrict__ okt,
                                                        int32_t* __restrict__ kept, R* __restrict__ endpoints,
-                                                       int32_t* __restrict__ status) {
+                                                       int32_t* __restrict__ status, const int32_t* __restrict__ n_rows) {
   __shared__ int s_scan[1024];
+  // with a device row count only its first rows exist (their groups were the only ones run)
+  int n_targets = stride_targets;
+  if (n_rows) {
+    P = min(P, (int)*n_rows);
+    n_targets = B + P * B;
+  }
   __shared__ int s_carry;
   __shared__ int s_pickfail;
   const int tid = threadIdx.x;
@@ -220,7 +229,7 @@ __global__ void __launch_bounds__(1024) k_lift_combine(const R* __restrict__ sol
     R bp = R(INFINITY);
     int bi = -1;
     for (int a = 0; a < n_draws; ++a) {
-      const int g = a * n_targets + t;
+      const int g = a * stride_targets + t;
       const bool dok = ik_ok[g] && pol_ok[g];
       const R pv = pen[g];
       if (dok && (!ok || pv < bp)) {

@@ -154,7 +154,7 @@ int launch_solve_al(const Traj& tr, const AlParams& prm, const R* values, int64_
 template <typename R>
 int launch_ik(const Traj& tr, int n_targets, int n_draws, uint64_t seed, uint64_t stride, int restarts, int max_iters,
               double damping, const double* tpos, const double* tyaw, const double* rows, int D, int polish,
-              int score_statics, IkOut out, cudaStream_t s) {
+              int score_statics, IkOut out, cudaStream_t s, const int32_t* n_rows) {
   if (n_targets <= 0) return SPASM_OK;
   SPASM_REQUIRE(restarts >= 1 && restarts <= 32, "restarts must be in [1, 32]");
   const int64_t groups = (int64_t)n_targets * n_draws;
@@ -162,10 +162,12 @@ int launch_ik(const Traj& tr, int n_targets, int n_draws, uint64_t seed, uint64_
   const int64_t grid = groups;
   if (bs <= 512 && grid <= kNumSMs)
     k_ik_group<R, 512><<<(unsigned)grid, bs, 0, s>>>(tr.dev<R>(), n_targets, n_draws, seed, stride, restarts,
-                                                     max_iters, damping, tpos, tyaw, rows, D, polish, score_statics, out);
+                                                     max_iters, damping, tpos, tyaw, rows, D, polish, score_statics, out,
+                                                     n_rows);
   else
     k_ik_group<R, 1024><<<(unsigned)grid, bs, 0, s>>>(tr.dev<R>(), n_targets, n_draws, seed, stride, restarts,
-                                                      max_iters, damping, tpos, tyaw, rows, D, polish, score_statics, out);
+                                                      max_iters, damping, tpos, tyaw, rows, D, polish, score_statics, out,
+                                                     n_rows);
   SPASM_CHECK_LAUNCH();
   return SPASM_OK;
 }
@@ -182,9 +184,9 @@ int launch_polish(const Traj& tr, R* Q, const double* tpos, const double* tyaw, 
 template <typename R>
 int launch_lift_combine(const R* sol, const uint8_t* ik_ok, const uint8_t* pol_ok, const R* pen, int n_targets,
                         int n_draws, int J, int B, int P, R* best, uint8_t* okt, int32_t* kept, R* endpoints,
-                        int32_t* status, cudaStream_t s) {
+                        int32_t* status, cudaStream_t s, const int32_t* n_rows) {
   k_lift_combine<R><<<1, 1024, 0, s>>>(sol, ik_ok, pol_ok, pen, n_targets, n_draws, J, B, P, best, okt, kept,
-                                       endpoints, status);
+                                       endpoints, status, n_rows);
   SPASM_CHECK_LAUNCH();
   return SPASM_OK;
 }

@@ -552,23 +552,88 @@ def ctypes_byref(x):
 _WS = _Workspace()
 
 
+def _warm_rows(warm_seeds, config, D):
+    if warm_seeds is None:
+        return None, 0
+    warm = np.atleast_2d(np.asarray(warm_seeds, dtype=float))
+    if warm.shape[0] == 0:
+        return None, 0
+    if warm.shape[0] > config.n:
+        raise ValueError("more seeds than particles")
+    if warm.shape[1] != D:
+        raise ValueError("seed dimension mismatch")
+    return np.ascontiguousarray(warm), warm.shape[0]
+
+
+class PendingSolve:
+    """A stage-1 solve launched on the device and not yet read back (``solve_launch``).
+
+    With a repeated shape the whole restart loop is one CUDA graph launch (a conditional
+    WHILE node; the success test runs on the device), so nothing waits for the host until
+    ``collect``. ``device_rows`` exposes the compacted result rows in device memory, so a
+    stage-2 consumer can read them in stream order without a round trip."""
+
+    def __init__(self, model, config, t0, warm):
+        self.model, self.config, self.t0 = model, config, t0
+        self._warm = warm  # kept alive until the launch has copied it
+
+    def device_rows(self):
+        """(rows pointer: float64 (p_return, D), count pointer: int32) on the device."""
+        rows = nat.c_void_p()
+        count = nat.c_void_p()
+        nat.check(nat.load().spasm_solve_device_rows(self.model.handle, nat.byref(rows), nat.byref(count)),
+                  "solve_device_rows")
+        return rows.value, count.value
+
+    def collect(self) -> "SolveResult":
+        config, D = self.config, self.model.dimension
+        parts = np.zeros((config.p_return, D))
+        costs = np.zeros(config.p_return)
+        idx = np.zeros(config.p_return, dtype=np.int64)
+        rep = nat.spasm_solve_report()
+        status = nat.check(nat.load().spasm_solve_collect(self.model.handle, nat.ptr(parts), nat.ptr(costs),
+                                                          nat.ptr(idx), ctypes_byref(rep)), "solve_collect")
+        return _result(status, rep, parts, costs, idx, self.t0, None)
+
+
+def _result(status, rep, parts, costs, idx, t0, trace_data):
+    k = int(rep.n_chosen) if status == nat.SPASM_OK else 0
+    report = SolveReport(
+        restarts=int(rep.restarts),
+        steps=int(rep.steps),
+        time_ms=(time.perf_counter() - t0) * 1e3,
+        n_satisfying=int(rep.n_satisfying),
+        flagged=int(rep.flagged),
+        trace=trace_data,
+        device_ms=float(rep.device_ms),
+        launches=int(rep.launches),
+    )
+    return SolveResult(success=bool(rep.success), particles=parts[:k].copy(), costs=costs[:k].copy(),
+                       indices=idx[:k].copy(), report=report)
+
+
+def solve_launch(model: NativeCostModel, config: OptimizerConfig, *, warm_seeds=None,
+                 sampler: str = "pcg64") -> PendingSolve:
+    """Start ``solve`` on the device and return without waiting (see PendingSolve)."""
+    if sampler not in _SAMPLERS:
+        raise ValueError(f"sampler must be one of {tuple(_SAMPLERS)}")
+    nat.require_cuda()
+    if not isinstance(model, NativeCostModel):
+        raise TypeError("solve_launch needs a native cost model")
+    t0 = time.perf_counter()
+    warm, n_warm = _warm_rows(warm_seeds, config, model.dimension)
+    cfg = config.native(_SAMPLERS[sampler], 0)
+    ws = _WS.get(model, cfg, n_warm)
+    nat.check(nat.load().spasm_solve_launch(model.handle, model.dtype_id, ctypes_byref(cfg), nat.ptr(warm), n_warm,
+                                            nat.ptr(ws), ws.numel(), nat.stream_handle()), "solve_launch")
+    return PendingSolve(model, config, t0, warm)
+
+
 def _solve_native(model: NativeCostModel, config: OptimizerConfig, warm_seeds, trace: bool, sampler: int):
     torch = _torch()
     t0 = time.perf_counter()
     D = model.dimension
-    warm = None
-    n_warm = 0
-    if warm_seeds is not None:
-        warm = np.atleast_2d(np.asarray(warm_seeds, dtype=float))
-        if warm.shape[0] > 0:
-            if warm.shape[0] > config.n:
-                raise ValueError("more seeds than particles")
-            if warm.shape[1] != D:
-                raise ValueError("seed dimension mismatch")
-            warm = np.ascontiguousarray(warm)
-            n_warm = warm.shape[0]
-        else:
-            warm = None
+    warm, n_warm = _warm_rows(warm_seeds, config, D)
     n_traced = min(config.m, TRACE_PARTICLE_CAP) if trace else 0
     cfg = config.native(sampler, n_traced)
     ws = _WS.get(model, cfg, n_warm)
@@ -595,19 +660,7 @@ def _solve_native(model: NativeCostModel, config: OptimizerConfig, warm_seeds, t
             costs=tc.double().cpu().numpy(),
             satisfied=ts.cpu().numpy().astype(bool),
         )
-    k = int(rep.n_chosen) if status == nat.SPASM_OK else 0
-    report = SolveReport(
-        restarts=int(rep.restarts),
-        steps=int(rep.steps),
-        time_ms=(time.perf_counter() - t0) * 1e3,
-        n_satisfying=int(rep.n_satisfying),
-        flagged=int(rep.flagged),
-        trace=trace_data,
-        device_ms=float(rep.device_ms),
-        launches=int(rep.launches),
-    )
-    return SolveResult(success=bool(rep.success), particles=parts[:k].copy(), costs=costs[:k].copy(),
-                       indices=idx[:k].copy(), report=report)
+    return _result(status, rep, parts, costs, idx, t0, trace_data)
 
 
 def _solve_generic(model: CostModel, config: OptimizerConfig, warm_seeds, trace: bool, sampler: int):

@@ -499,10 +499,19 @@ class _LiftDevice:
         self.P = P
 
 
-def _lift_async(geo: _Geometry, placements_dev, seed: int, candidates: int, precision: str) -> _LiftDevice:
+def _lift_async(geo: _Geometry, placements_dev, seed: int, candidates: int, precision: str, *,
+                device_rows=None) -> _LiftDevice:
+    """Enqueue lift_placements. ``placements_dev`` is a (P, D) float64 CUDA tensor, or None
+    with ``device_rows = (rows pointer, count pointer, P)``: the stage-1 result read in place
+    (particle_opt.PendingSolve.device_rows), only its first *count rows exist."""
     torch = _torch()
     dt = _check_precision(precision)
-    P, D = placements_dev.shape
+    if device_rows is not None:
+        rows_ptr, n_rows_ptr, P = device_rows
+        D = geo.row_dim
+    else:
+        P, D = placements_dev.shape
+        rows_ptr, n_rows_ptr = nat.ptr(placements_dev), None
     if D != geo.row_dim:
         raise ValueError(f"placement rows have dimension {D}, expected {geo.row_dim}")
     B, J = geo.n_segments, geo.dof
@@ -511,7 +520,7 @@ def _lift_async(geo: _Geometry, placements_dev, seed: int, candidates: int, prec
     ends = torch.empty((P, B, 2, J), dtype=_tdtype(precision), device="cuda")
     kept = torch.empty(max(P, 1), dtype=torch.int32, device="cuda")
     status = torch.empty(2, dtype=torch.int32, device="cuda")
-    nat.check(geo._lib.spasm_lift(geo.handle, dt, nat.ptr(placements_dev), P, D, int(seed), int(candidates),
+    nat.check(geo._lib.spasm_lift(geo.handle, dt, rows_ptr, P, n_rows_ptr, D, int(seed), int(candidates),
                                   nat.ptr(ws), ws_bytes, nat.ptr(ends), nat.ptr(kept), nat.ptr(status), _stream()),
               "spasm_lift")
     return _LiftDevice(ends, kept, status, P)
@@ -750,9 +759,15 @@ def _trajopt_config(scene, overrides) -> TrajOptConfig:
     return TrajOptConfig(**merged)
 
 
-def solve_stage2(scene, result, config, seed, trajopt_overrides, t0, precision: str = "fp32"):
-    """lift -> init -> AL solve with device-resident intermediates and one host sync
-    (the AL result block); then the independent validation outside the timed span."""
+def solve_stage2(scene, result, config, seed, trajopt_overrides, t0, precision: str = "fp32", *, pending=None):
+    """lift -> init -> AL solve with device-resident intermediates and one host sync (the AL
+    result block); then the independent validation outside the timed span.
+
+    With ``pending`` (a launched, uncollected stage-1 solve: particle_opt.PendingSolve) the
+    lift reads the stage-1 rows in place on the device, the whole chain is enqueued behind
+    the stage-1 graph, and stage 1 is collected only after the AL result: one host sync for
+    the whole pipeline. Returns (SceneSolution or None, stage-1 SolveResult); None when
+    stage 1 found nothing (the caller reports that failure)."""
     import time
 
     from .bench_api import SceneSolution
@@ -762,27 +777,36 @@ def solve_stage2(scene, result, config, seed, trajopt_overrides, t0, precision: 
     lift_geo = _geometry(scene.problem, scene.chain, scene.grasp, scene.obstacle_centers, scene.obstacle_radii,
                          default_statics=False)
     geo = _geometry(scene.problem, scene.chain, scene.grasp, scene.obstacle_centers, scene.obstacle_radii)
-    pl = torch.as_tensor(np.ascontiguousarray(result.particles, dtype=float)).to("cuda", non_blocking=True)
-    lift = _lift_async(lift_geo, pl, seed, LIFT_CANDIDATES, precision)
+    if pending is not None:
+        rows_ptr, n_ptr = pending.device_rows()
+        lift = _lift_async(lift_geo, None, seed, LIFT_CANDIDATES, precision,
+                           device_rows=(rows_ptr, n_ptr, config.p_return))
+    else:
+        pl = torch.as_tensor(np.ascontiguousarray(result.particles, dtype=float)).to("cuda", non_blocking=True)
+        lift = _lift_async(lift_geo, pl, seed, LIFT_CANDIDATES, precision)
     state = _pcg_state(trajectory_stream(seed))
     values = _init_async(geo, lift.endpoints, lift.status[1:], tcfg, state, precision)
     status, res, best, report = _solve_al_device(geo, values, tcfg, None, precision, n_active=lift.status[1:],
                                                  lift_status=lift.status, want_report=False)
+    if pending is not None:
+        result = pending.collect()  # already complete: the AL result came after it in stream order
+        if not result.success:
+            return None, result
     time_ms = (time.perf_counter() - t0) * 1e3
+    n_lift = lift.P * geo.n_segments + geo.n_segments
     stats = {"stage2_particles": int(res.n_particles), "stage2_outers": int(res.n_outers),
              "stage2_iterations": int(res.n_particles) * int(res.n_outers) * int(tcfg.inner_steps),
-             "stage2_launches": 6, "al_device_ms": float(res.device_ms), "lift_targets": len(pl) * geo.n_segments
-             + geo.n_segments}
+             "stage2_launches": 6, "al_device_ms": float(res.device_ms), "lift_targets": n_lift}
     if status == nat.SPASM_LIFT_FAILURE:
         return SceneSolution(False, time_ms, result.report.restarts, result.report.steps, math.nan, stats=stats,
-                             bookkeeping={"lift_failed": True})
+                             bookkeeping={"lift_failed": True}), result
     kept = lift.kept[:int(res.n_particles)].cpu().numpy()
     book = {"kept": kept, "accepted_outer": int(res.accepted_outer), "al_particle": int(res.particle_index),
             "objective": float(res.objective), "lift_failed": False}
     if status == nat.SPASM_AL_FAILURE:
         w = float(res.least_violation)
         return SceneSolution(False, time_ms, result.report.restarts, result.report.steps, w, max_violation=w,
-                             stats=stats, bookkeeping=book)
+                             stats=stats, bookkeeping=book), result
     traj = _particle_trajectory(best.double().cpu().numpy(), geo)
     feasible, worst = validate(traj, scene.problem, scene.chain, grasp=scene.grasp,
                                static_centers=scene.obstacle_centers, static_radii=scene.obstacle_radii,
@@ -790,7 +814,7 @@ def solve_stage2(scene, result, config, seed, trajopt_overrides, t0, precision: 
     return SceneSolution(bool(feasible), time_ms, result.report.restarts, result.report.steps, worst,
                          placement=np.asarray(result.particles)[int(kept[res.particle_index])].copy(),
                          trajectory=traj, path_length=trajectory_path_length(traj), max_violation=worst, stats=stats,
-                         bookkeeping=book)
+                         bookkeeping=book), result
 
 
 def solve_motion_scene(scene, seed, trajopt_overrides, precision: str = "fp32"):
