@@ -216,9 +216,29 @@ int spasm_shard_select(const spasm_model* model, int dtype, const spasm_solve_co
                        int64_t n_local, const double* warm_dev, int64_t n_warm, void* workspace,
                        int64_t workspace_bytes, uint64_t* elite, int32_t* launches, void* stream);
 int spasm_shard_descend(const spasm_model* model, int dtype, const spasm_solve_config* cfg, int restart,
-                        const uint64_t* elite_all, int world, int64_t pos_lo, int64_t pos_hi, const double* warm_dev,
-                        int64_t n_warm, void* workspace, int64_t workspace_bytes, double* candidates,
-                        int32_t* launches, void* stream);
+                        const uint64_t* elite_all, int world, int64_t run_len, int64_t pos_lo, int64_t pos_hi,
+                        const double* warm_dev, int64_t n_warm, void* workspace, int64_t workspace_bytes,
+                        double* candidates, int32_t* launches, void* stream);
+/* Exact distributed top-m selection (replaces the all-gather of m records per rank when that
+ * gather is large): after spasm_shard_select (elite may then be NULL), per 8-bit key digit
+ * (4 for F32, 8 for F64) spasm_shard_topm_hist counts the rank's keys per digit value under
+ * the agreed prefix (256 int64), the caller all-reduces (sums) the counts over the ranks and
+ * spasm_shard_topm_pick extends the prefix (state: spasm_shard_topm_state_bytes, set up by
+ * spasm_shard_topm_init with m). spasm_shard_topm_local then gives the rank's
+ * {records below K*, records at K*, K* records the top m takes}; the caller allots the ties
+ * to the lowest ranks (lowest global rows) and spasm_shard_topm_contrib writes the rank's
+ * first `take` sorted (key, row) records padded to `cap` (the largest take over the ranks);
+ * the gathered contributions (m records in total) go to spasm_shard_descend with
+ * run_len = cap. Same result as the all-gather protocol, bit for bit. */
+int64_t spasm_shard_topm_state_bytes(void);
+int spasm_shard_topm_init(int dtype, int64_t m, void* state, void* stream);
+int spasm_shard_topm_hist(const spasm_model* model, int dtype, const spasm_solve_config* cfg, int64_t n_local,
+                          void* workspace, const void* state, int64_t* hist, void* stream);
+int spasm_shard_topm_pick(void* state, const int64_t* hist_sum, void* stream);
+int spasm_shard_topm_local(const spasm_model* model, int dtype, const spasm_solve_config* cfg, int64_t n_local,
+                           void* workspace, const void* state, int64_t* counts, void* stream);
+int spasm_shard_topm_contrib(const spasm_model* model, int dtype, const spasm_solve_config* cfg, int64_t n_local,
+                             void* workspace, int64_t take, int64_t cap, uint64_t* records, void* stream);
 
 /* =====================================================================================
  * Stage 2: trajectory optimization (reference trajopt.py / robot.py)

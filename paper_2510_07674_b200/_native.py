@@ -203,9 +203,19 @@ SIGNATURES = {
     ),
     "spasm_shard_descend": (
         c_int,
-        [c_void_p, c_int, POINTER(spasm_solve_config), c_int, c_void_p, c_int, c_int64, c_int64, c_void_p, c_int64,
-         c_void_p, c_int64, c_void_p, c_void_p, c_void_p],
+        [c_void_p, c_int, POINTER(spasm_solve_config), c_int, c_void_p, c_int, c_int64, c_int64, c_int64, c_void_p,
+         c_int64, c_void_p, c_int64, c_void_p, c_void_p, c_void_p],
     ),
+    "spasm_shard_topm_state_bytes": (c_int64, []),
+    "spasm_shard_topm_init": (c_int, [c_int, c_int64, c_void_p, c_void_p]),
+    "spasm_shard_topm_hist": (
+        c_int, [c_void_p, c_int, POINTER(spasm_solve_config), c_int64, c_void_p, c_void_p, c_void_p, c_void_p]),
+    "spasm_shard_topm_pick": (c_int, [c_void_p, c_void_p, c_void_p]),
+    "spasm_shard_topm_local": (
+        c_int, [c_void_p, c_int, POINTER(spasm_solve_config), c_int64, c_void_p, c_void_p, c_void_p, c_void_p]),
+    "spasm_shard_topm_contrib": (
+        c_int, [c_void_p, c_int, POINTER(spasm_solve_config), c_int64, c_void_p, c_int64, c_int64, c_void_p,
+                c_void_p]),
     "spasm_traj_create": (c_int, [POINTER(c_void_p), POINTER(spasm_chain), POINTER(spasm_traj_desc)]),
     "spasm_traj_destroy": (None, [c_void_p]),
     "spasm_traj_segments": (c_int, [c_void_p]),

@@ -7,7 +7,11 @@ of the ONE centralized draw of the restart (particle_opt.py:176-192). Per restar
 
 1. ``spasm_shard_select`` (device): sample + LINEAR-evaluate the rank's rows, stable-sort
    them, emit the rank's elite run (m records ``(order key, global row)``).
-2. all-gather of the elite runs (m x 16 B per rank; the only large exchange).
+2. all-gather of the elite runs (m x 16 B per rank). When that gather is large
+   (world x m x 16 B > SELECT_PROTOCOL_BYTES) the exact distributed top-m select replaces
+   it (``topm_exchange``): an MSB-first radix select of the global m-th key over
+   all-reduced 256-bin digit counts, then each rank contributes only its records of the
+   global top m (m records in total instead of world x m).
 3. ``spasm_shard_descend`` (device): exact merge of the runs into the global stable top-m
    (particle_opt.py:195-200), re-draw of the rank's slice of it, fused descent schedule
    (particle_opt.py:266-300), satisfying ordering and re-check (particle_opt.py:359-366).
@@ -64,6 +68,19 @@ class TorchComm:
         self.world = dist.get_world_size(group) if self.active else 1
         self.backend = dist.get_backend(group) if self.active else None
 
+    def all_reduce_sum(self, t):
+        """Elementwise sum over the ranks (t's device; gloo stages through host memory)."""
+        if self.world == 1:
+            return t
+        import torch.distributed as dist
+
+        if self.backend == "nccl":
+            dist.all_reduce(t, op=dist.ReduceOp.SUM, group=self.group)
+            return t
+        src = t.detach().cpu().contiguous()
+        dist.all_reduce(src, op=dist.ReduceOp.SUM, group=self.group)
+        return src.to(t.device)
+
     def all_gather(self, t):
         """(world, *t.shape) tensor on t's device, rank-major."""
         torch = _torch()
@@ -104,29 +121,107 @@ class NativeShardOps:
         self.ws = torch.empty(max(1, nbytes), dtype=torch.uint8, device="cuda")
         self.launches = 0
 
-    def select(self, restart: int, row_lo: int, n_local: int):
+    @property
+    def key_bits(self) -> int:
+        return 32 if self.model.dtype_id == nat.F32 else 64
+
+    def select(self, restart: int, row_lo: int, n_local: int, elite: bool = True):
+        """Sample + evaluate + sort the rank's rows; with ``elite`` also emit its elite run
+        (all-gather protocol); the top-m select protocol reads the sorted keys in place."""
         torch = _torch()
-        elite = torch.empty((self.m, 2), dtype=torch.int64, device="cuda")
+        self.n_local = n_local
+        out = torch.empty((self.m, 2), dtype=torch.int64, device="cuda") if elite else None
         nl = nat.c_int32(0)
         nat.check(self.lib.spasm_shard_select(self.model.handle, self.model.dtype_id, ctypes_byref(self.cfg), restart,
                                               row_lo, n_local, nat.ptr(self.warm), self.n_warm, nat.ptr(self.ws),
-                                              self.ws.numel(), nat.ptr(elite), ctypes_byref(nl),
+                                              self.ws.numel(), nat.ptr(out), ctypes_byref(nl),
                                               nat.stream_handle()), "shard_select")
         self.launches += nl.value
-        return elite
+        return out
 
-    def descend(self, restart: int, elite_all, pos_lo: int, pos_hi: int):
+    def topm_init(self):
         torch = _torch()
-        world = elite_all.shape[0]
+        st = torch.empty(int(self.lib.spasm_shard_topm_state_bytes()), dtype=torch.uint8, device="cuda")
+        nat.check(self.lib.spasm_shard_topm_init(self.model.dtype_id, self.m, nat.ptr(st), nat.stream_handle()),
+                  "shard_topm_init")
+        return st
+
+    def topm_hist(self, st):
+        torch = _torch()
+        h = torch.empty(256, dtype=torch.int64, device="cuda")
+        nat.check(self.lib.spasm_shard_topm_hist(self.model.handle, self.model.dtype_id, ctypes_byref(self.cfg),
+                                                 self.n_local, nat.ptr(self.ws), nat.ptr(st), nat.ptr(h),
+                                                 nat.stream_handle()), "shard_topm_hist")
+        self.launches += 1
+        return h
+
+    def topm_pick(self, st, hist_sum):
+        nat.check(self.lib.spasm_shard_topm_pick(nat.ptr(st), nat.ptr(hist_sum.contiguous()), nat.stream_handle()),
+                  "shard_topm_pick")
+        self.launches += 1
+
+    def topm_local(self, st):
+        torch = _torch()
+        c = torch.empty(3, dtype=torch.int64, device="cuda")
+        nat.check(self.lib.spasm_shard_topm_local(self.model.handle, self.model.dtype_id, ctypes_byref(self.cfg),
+                                                  self.n_local, nat.ptr(self.ws), nat.ptr(st), nat.ptr(c),
+                                                  nat.stream_handle()), "shard_topm_local")
+        self.launches += 1
+        return c
+
+    def topm_contrib(self, take: int, cap: int):
+        torch = _torch()
+        rec = torch.empty((cap, 2), dtype=torch.int64, device="cuda")
+        nat.check(self.lib.spasm_shard_topm_contrib(self.model.handle, self.model.dtype_id, ctypes_byref(self.cfg),
+                                                    self.n_local, nat.ptr(self.ws), take, cap, nat.ptr(rec),
+                                                    nat.stream_handle()), "shard_topm_contrib")
+        self.launches += 1
+        return rec
+
+    def descend(self, restart: int, runs, pos_lo: int, pos_hi: int):
+        """``runs``: (world, run_len, 2) gathered records (elite runs or top-m contributions)."""
+        torch = _torch()
+        world, run_len = runs.shape[0], runs.shape[1]
         cand = torch.empty(3 + self.p * (4 + self.D), dtype=torch.float64, device="cuda")
         nl = nat.c_int32(0)
         nat.check(self.lib.spasm_shard_descend(self.model.handle, self.model.dtype_id, ctypes_byref(self.cfg),
-                                               restart, nat.ptr(elite_all.contiguous()), world, pos_lo, pos_hi,
+                                               restart, nat.ptr(runs.contiguous()), world, run_len, pos_lo, pos_hi,
                                                nat.ptr(self.warm), self.n_warm, nat.ptr(self.ws), self.ws.numel(),
                                                nat.ptr(cand), ctypes_byref(nl), nat.stream_handle()),
                   "shard_descend")
         self.launches += nl.value
         return cand
+
+
+# the top-m select protocol replaces the all-gather of m records per rank once that gather
+# exceeds this many bytes (below it, one collective beats the key_bits/8 + 2 small ones)
+SELECT_PROTOCOL_BYTES = 4 << 20
+
+
+def allot_top_m(counts: np.ndarray) -> np.ndarray:
+    """Per-rank record counts of the global top m from the gathered (world, 3) rows
+    (records below K*, records at K*, K* records the top m takes): every rank contributes
+    its records below the threshold key and the K*-keyed ties go to the lowest global rows,
+    i.e. to the lower ranks first (contiguous row shards)."""
+    counts = np.asarray(counts, dtype=np.int64).reshape(-1, 3)
+    less, ties, need = counts[:, 0], counts[:, 1], int(counts[0, 2])
+    before = np.concatenate([[0], np.cumsum(ties)[:-1]])
+    return less + np.clip(need - before, 0, ties)
+
+
+def topm_exchange(ops, comm, restart: int, row_lo: int, n_local: int, m: int):
+    """The exact distributed top-m selection of one restart (spasm_shard_topm_*): key_bits/8
+    all-reduces of 256 counts, one all-gather of 3 counts, one all-gather of the rank's
+    contribution (m records over all ranks). Returns (world, cap, 2) runs for descend."""
+    ops.select(restart, row_lo, n_local, elite=False)
+    st = ops.topm_init()
+    for _ in range(ops.key_bits // 8):
+        h = comm.all_reduce_sum(ops.topm_hist(st))
+        ops.topm_pick(st, h)
+    take = allot_top_m(comm.all_gather(ops.topm_local(st)).cpu().numpy())
+    assert int(take.sum()) == m, (take, m)
+    cap = max(1, int(take.max()))
+    return comm.all_gather(ops.topm_contrib(int(take[comm.rank]), cap)).reshape(comm.world, cap, 2)
 
 
 def merge_candidates(blocks: np.ndarray, D: int, p_return: int, epsilon: float):
@@ -153,7 +248,7 @@ def merge_candidates(blocks: np.ndarray, D: int, p_return: int, epsilon: float):
 
 
 def solve_sharded(cost_model, config: OptimizerConfig, *, group=None, comm=None, ops=None, warm_seeds=None,
-                  sampler: str = "pcg64") -> SolveResult:
+                  sampler: str = "pcg64", protocol: str = "auto") -> SolveResult:
     """``particle_opt.solve`` (reference particle_opt.py:303-400) over all ranks of ``group``.
 
     Every rank must call it with the same model, config and warm seeds; every rank returns
@@ -187,10 +282,17 @@ def solve_sharded(cost_model, config: OptimizerConfig, *, group=None, comm=None,
     steps = flagged_total = 0
     per = config.k_lin + config.k_quad
     result = None
+    if protocol not in ("auto", "gather", "select"):
+        raise ValueError("protocol must be 'auto', 'gather' or 'select'")
+    use_select = protocol == "select" or (protocol == "auto" and comm.world > 1
+                                          and comm.world * config.m * 16 > SELECT_PROTOCOL_BYTES)
     for restart in range(config.max_restarts):
-        elite = ops.select(restart, row_lo, row_hi - row_lo)
-        elite_all = comm.all_gather(elite).reshape(comm.world, config.m, 2)
-        cand = ops.descend(restart, elite_all, pos_lo, pos_hi)
+        if use_select:
+            runs = topm_exchange(ops, comm, restart, row_lo, row_hi - row_lo, config.m)
+        else:
+            elite = ops.select(restart, row_lo, row_hi - row_lo)
+            runs = comm.all_gather(elite).reshape(comm.world, config.m, 2)
+        cand = ops.descend(restart, runs, pos_lo, pos_hi)
         blocks = comm.all_gather(cand).cpu().numpy()
         steps += per
         n_sat, flagged, chosen = merge_candidates(blocks, D, config.p_return, config.epsilon)
@@ -216,4 +318,5 @@ def solve_sharded(cost_model, config: OptimizerConfig, *, group=None, comm=None,
                        indices=chosen[:, 1].astype(np.int64), report=report)
 
 
-__all__ = ["TorchComm", "NativeShardOps", "merge_candidates", "shard_range", "solve_sharded", "torch_dtype"]
+__all__ = ["TorchComm", "NativeShardOps", "SELECT_PROTOCOL_BYTES", "allot_top_m", "merge_candidates", "shard_range",
+           "solve_sharded", "topm_exchange", "torch_dtype"]

@@ -25,7 +25,7 @@ def order_key64(c):
 
 
 def merge_runs(runs, m):
-    """Global first m rows of the gathered (world, m, 2) records (lexicographic key, row)."""
+    """Global first m rows of the gathered (world, run_len, 2) records (lexicographic key, row)."""
     r = np.asarray(runs).reshape(-1, 2).view(np.uint64)
     r = r[r[:, 1] != ALL_ONES]
     order = np.lexsort((r[:, 1], r[:, 0]))[:m]
@@ -48,15 +48,57 @@ class OracleShardOps:
             self._draws = {restart: v}
         return self._draws[restart]
 
-    def select(self, restart, row_lo, n_local):
+    key_bits = 64
+
+    def select(self, restart, row_lo, n_local, elite=True):
         v = self._batch(restart)[row_lo: row_lo + n_local]
         m = self.cfg.m
+        c = self.o.evaluate(v, orc.LINEAR) if n_local else np.zeros(0)
+        order = np.argsort(c, kind="stable")
+        self._keys = order_key64(c[order])  # the rank's sorted (key, global row) records
+        self._rows = (row_lo + order).astype(np.uint64)
+        if not elite:
+            return None
         rec = np.full((m, 2), ALL_ONES, dtype=np.uint64)
-        if n_local:
-            c = self.o.evaluate(v, orc.LINEAR)
-            order = np.argsort(c, kind="stable")[:m]
-            rec[: len(order), 0] = order_key64(c[order])
-            rec[: len(order), 1] = (row_lo + order).astype(np.uint64)
+        k = min(m, n_local)
+        rec[:k, 0] = self._keys[:k]
+        rec[:k, 1] = self._rows[:k]
+        return torch.from_numpy(rec.view(np.int64).copy())
+
+    # the top-m select protocol (spasm_shard_topm_*), on the rank's sorted keys
+    def topm_init(self):
+        return {"prefix": 0, "remaining": self.cfg.m, "pass": 0}
+
+    def topm_hist(self, st):
+        shift = self.key_bits - 8 * (st["pass"] + 1)
+        k = self._keys.astype(object)
+        sel = [int(x) for x in k if (int(x) >> (shift + 8)) == (st["prefix"] >> (shift + 8))]
+        h = np.zeros(256, dtype=np.int64)
+        for x in sel:
+            h[(x >> shift) & 0xFF] += 1
+        return torch.from_numpy(h)
+
+    def topm_pick(self, st, hist_sum):
+        h = np.asarray(hist_sum.cpu().numpy() if hasattr(hist_sum, "cpu") else hist_sum, dtype=np.int64)
+        shift = self.key_bits - 8 * (st["pass"] + 1)
+        rem, d = st["remaining"], 0
+        while d < 255 and rem > h[d]:
+            rem -= h[d]
+            d += 1
+        st["prefix"] |= d << shift
+        st["remaining"] = int(rem)
+        st["pass"] += 1
+
+    def topm_local(self, st):
+        ks = np.uint64(st["prefix"])
+        less = int(np.searchsorted(self._keys, ks, side="left"))
+        ties = int(np.searchsorted(self._keys, ks, side="right")) - less
+        return torch.tensor([less, ties, st["remaining"]], dtype=torch.int64)
+
+    def topm_contrib(self, take, cap):
+        rec = np.full((cap, 2), ALL_ONES, dtype=np.uint64)
+        rec[:take, 0] = self._keys[:take]
+        rec[:take, 1] = self._rows[:take]
         return torch.from_numpy(rec.view(np.int64).copy())
 
     def descend(self, restart, elite_all, pos_lo, pos_hi):

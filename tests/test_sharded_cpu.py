@@ -60,7 +60,7 @@ def _worker(rank, world, init_file, case, out_path):
         cfg = OptimizerConfig(**kw)
         warm = case.get("warm")
         ops = OracleShardOps(o, ocfg, warm)
-        res = solve_sharded(o, cfg, comm=TorchComm(), ops=ops, warm_seeds=warm)
+        res = solve_sharded(o, cfg, comm=TorchComm(), ops=ops, warm_seeds=warm, protocol=case.get("protocol", "auto"))
         if rank == 0:
             np.savez(out_path, success=res.success, restarts=res.report.restarts, indices=res.indices,
                      particles=res.particles, costs=res.costs, n_sat=res.report.n_satisfying,
@@ -91,10 +91,12 @@ CASES = [
 ]
 
 
+@pytest.mark.parametrize("protocol", ["gather", "select"])
 @pytest.mark.parametrize("world", [2, 3])
 @pytest.mark.parametrize("ci", range(len(CASES)))
-def test_sharded_solve_matches_single_process_reference(world, ci):
+def test_sharded_solve_matches_single_process_reference(world, ci, protocol):
     case = dict(CASES[ci])
+    case["protocol"] = protocol
     scene = load_scene(case["scene"])
     o = orc.oracle_model(scene.problem)
     kw = {**scene.solver_overrides, **case["over"]}
@@ -112,3 +114,13 @@ def test_sharded_solve_matches_single_process_reference(world, ci):
     np.testing.assert_array_equal(got["indices"], ref.indices)
     np.testing.assert_array_equal(got["particles"], ref.particles)
     np.testing.assert_array_equal(got["costs"], ref.costs)
+
+
+def test_allot_top_m_gives_ties_to_lower_ranks():
+    from paper_2510_07674_b200.sharded import allot_top_m
+
+    # rows: (below K*, at K*, K* records taken overall); 10 records at K* across ranks, 4 taken
+    counts = np.array([[3, 2, 4], [5, 0, 4], [1, 6, 4], [0, 2, 4]])
+    take = allot_top_m(counts)
+    assert take.tolist() == [3 + 2, 5, 1 + 2, 0]
+    assert int(take.sum()) == 3 + 5 + 1 + 4
