@@ -37,6 +37,9 @@ METRIC = "solve time ms (p50) at 100% success; particle-iterations/sec at 1/2/4/
 WORKLOADS = {
     "c1": ("single1", {}, False,
            "C1 7-DOF arm, single-block pick-and-place, 1024 particles, stage 1 + stage 2 (32 waypoints)"),
+    "c1f": ("single1f", {}, False,
+            "C1 with the Franka-like explicit 7-DOF chain (Panda link offsets / limits, 11 collision spheres), "
+            "single-block pick-and-place, 1024 particles, stage 1 + stage 2 (32 waypoints)"),
     "c2": ("tower3c", {}, False,
            "C2 3-block stacking with cuboid obstacles, 16k particles, stage 1 + stage 2; cuboids 0.2x0.2x0.3 m and "
            "0.1x0.1x0.2 m as grids of r=0.05 m spheres at 0.1 m pitch (2x2x3 + 1x1x2 = 14 obstacle spheres)"),
@@ -437,7 +440,7 @@ def run_b200(args, workload=None, sub=False):
 
 # workload -> key prefix of the reference's own per-seed pipeline outcomes
 # (tests/golden/pipeline_reference.json, made by tests/golden/make_golden_pipeline.py)
-_REF_OUTCOME_KEYS = {"c3p": "tetris5@64k", "c2": "tower3c", "c1": "single1"}
+_REF_OUTCOME_KEYS = {"c3p": "tetris5@64k", "c2": "tower3c", "c1": "single1", "c1f": "single1f"}
 
 
 def _reference_outcomes(workload, seeds, sols):
@@ -649,13 +652,14 @@ def main():
         return
     if args.gpus == 1 and dist_env()[1] == 1 and args.workload == "c2" and not args.no_sub:
         # same-process sub-records of the other headline configs (C5: the particle-iterations/s
-        # clause at 1M particles and k_schedule_tile's FP32 roofline; C3: 64k tetris5), each
-        # with its own clocks / roofline, so the driver's default run carries them
+        # clause at 1M particles and k_schedule_tile's FP32 roofline; C3: 64k tetris5; C1 with
+        # the builtin arm and with the Franka-like chain), each with its own clocks / roofline,
+        # so the driver's default run carries them
         line["sub_records"] = {}
-        for w in ("c5", "c3"):
+        for w in ("c5", "c3", "c1", "c1f"):
             sub = run_b200(args, workload=w, sub=True)
             keep = ("value", "unit", "ms_per_step", "p50_solve_ms", "p50_step_ms", "success_rate", "steps", "warmup",
-                    "config", "e2e", "roofline", "clocks", "gpu_launches", "breakdown")
+                    "config", "e2e", "roofline", "clocks", "gpu_launches", "breakdown", "reference_outcomes")
             line["sub_records"][w] = {k: sub[k] for k in keep if k in sub}
     if args.gpus == 1 and dist_env()[1] == 1 and args.workload == "c3p" and not args.no_sub:
         # C3's 4- and 6-object variants (stage 1 at 64k) beside the 5-object full pipeline

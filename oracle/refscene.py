@@ -20,6 +20,18 @@ def ref_scene(name_or_dict):
         d = our_scenes.BUNDLED[name_or_dict]()
     else:
         d = dict(name_or_dict)
+    if "obstacles" in d:
+        # this repo's cuboid entries -> the reference schema's explicit sphere sets (same
+        # local grid, same pose transform, loader.py:157-177)
+        from paper_2510_07674_b200.problems.loader import cuboid_spheres
+
+        obs = []
+        for e in d["obstacles"]:
+            if "cuboid" in e:
+                c, r = cuboid_spheres(e["cuboid"]["size"], e["cuboid"]["sphere_radius"])
+                e = {"centers": c.tolist(), "radii": r.tolist(), "pose": list(e["pose"])}
+            obs.append(e)
+        d["obstacles"] = obs
     tight = d.pop("tight_packing", True)
     if tight:
         return load_scene(d)

@@ -6,6 +6,7 @@ problems by name; the rest are the BASELINE.json configurations mapped onto the
 reference's problem families:
 
   single1      C1  1 block, 7-DOF arm, stage 1 + stage 2 with T = 32 waypoints
+  single1f     C1  the same with the Franka-like explicit 7-DOF chain (franka_like_robot)
   tower3c      C2  3-block stacking with cuboid obstacles (cuboids as sphere grids)
   tetris4/6    C3  4- and 6-tetromino tight packings (tetris5 is the 5-block case)
   tower6r      C4  6-block rearrangement with a moving sphere obstacle (reactive)
@@ -100,12 +101,40 @@ def tower4():
     }
 
 
-def cuboid_obstacle(center, size, radius):
-    """A cuboid approximated by a grid of spheres of the given radius (schema obstacle entry)."""
-    counts = [max(1, int(round(s / (2 * radius)))) for s in size]
-    axes = [np.linspace(-s / 2 + radius, s / 2 - radius, n) if n > 1 else np.zeros(1) for s, n in zip(size, counts)]
-    pts = np.stack(np.meshgrid(*axes, indexing="ij"), axis=-1).reshape(-1, 3) + np.asarray(center)
-    return {"centers": pts.tolist(), "radii": [radius] * len(pts)}
+def cuboid_obstacle(center, size, radius, yaw=0.0):
+    """A cuboid obstacle entry of the scene schema (loader: ``{"cuboid": {"size",
+    "sphere_radius"}, "pose"}``), compiled by the loader to a grid of spheres."""
+    return {"cuboid": {"size": [float(v) for v in size], "sphere_radius": float(radius)},
+            "pose": [float(center[0]), float(center[1]), float(center[2]), float(yaw)]}
+
+
+def franka_like_robot():
+    """Explicit 7-DOF chain with the Franka Panda's link offsets (0.333 / 0.316 / 0.0825 /
+    0.384 / 0.088 m), joint limits and z-y-z-(-y)-z-y-z axis pattern in the reference's
+    translate-then-rotate model (robot.py:120-141; the loader's explicit-chain schema,
+    loader.py:209-251, identity tool rotation), a 0.21 m flange + hand tool along the last
+    link's z, and 11 collision spheres (BASELINE configs[0]: "Franka Panda 7-DOF")."""
+    joints = [
+        ([0, 0, 1], [0, 0, 0.333], [-2.8973, 2.8973]),
+        ([0, 1, 0], [0, 0, 0], [-1.7628, 1.7628]),
+        ([0, 0, 1], [0, 0, 0.316], [-2.8973, 2.8973]),
+        ([0, -1, 0], [0.0825, 0, 0], [-3.0718, -0.0698]),
+        ([0, 0, 1], [-0.0825, 0, 0.384], [-2.8973, 2.8973]),
+        ([0, 1, 0], [0, 0, 0], [-0.0175, 3.7525]),
+        ([0, 0, 1], [0.088, 0, 0], [-2.8973, 2.8973]),
+    ]
+    spheres = [
+        [([0, 0, -0.18], 0.08)],                                  # base column
+        [([0, 0, 0.12], 0.07), ([0, 0, 0.24], 0.07)],             # upper arm
+        [([0.04, 0, 0.0], 0.07)],                                 # elbow
+        [([-0.04, 0, 0.12], 0.06), ([-0.08, 0, 0.26], 0.06)],     # forearm
+        [([0, 0, 0.0], 0.06)],                                    # wrist 1
+        [([0.044, 0, 0.0], 0.06)],                                # wrist 2
+        [([0, 0, 0.07], 0.055), ([0, 0, 0.13], 0.05)],            # flange + hand
+    ]
+    return {"joints": [{"axis": a, "offset": o, "limits": l} for a, o, l in joints],
+            "link_spheres": [[{"center": c, "radius": r} for c, r in link] for link in spheres],
+            "tool": {"translation": [0.0, 0.0, 0.2104]}}
 
 
 def tower3c():
@@ -153,6 +182,15 @@ def single1():
     }
 
 
+def single1f():
+    """C1 with the Franka-like explicit 7-DOF chain (franka_like_robot) instead of the
+    builtin spatial arm; same block, table region and T = 32 waypoints."""
+    d = single1()
+    d["name"] = "single1f"
+    d["robot"] = franka_like_robot()
+    return d
+
+
 def corridor3():
     return {"problem_type": "motion", "name": "corridor3", "robot": {"builtin": "planar3"},
             "start": [-1.1, 0.6, 0.3], "goal": [1.1, -0.6, -0.3],
@@ -167,5 +205,5 @@ def empty3():
 BUNDLED = {
     "domino2": domino2, "tetris5": tetris5, "tetris8": tetris8, "tower4": tower4, "corridor3": corridor3,
     "empty3": empty3, "tetris4": tetris4, "tetris6": tetris6, "tower3c": tower3c, "tower6r": tower6r,
-    "single1": single1,
+    "single1": single1, "single1f": single1f,
 }
