@@ -574,7 +574,7 @@ def cpu_baseline(args, workload=None, budget_s=20.0):
     def sample(th, budget, max_solves):
         its, t_total, times = 0, 0.0, []
         t_start = time.perf_counter()
-        while time.perf_counter() - t_start < budget and len(times) < max_solves:
+        while len(times) < max_solves and (not times or time.perf_counter() - t_start < budget):
             r = _cpu_solve(scene, scene_name, over, stage1_only, len(times), th, max_restarts=mr)
             t_total += r.time_ms * 1e-3
             times.append(r.time_ms)
