@@ -27,6 +27,7 @@
 // Reference: trajopt.py:396-653 (value + gradient), 936-1063 (solve), 1071-1153 (validate).
 #pragma once
 #include "coop.cuh"
+#include "f32x2.cuh"
 #include "stage1_models.cuh"
 #include "twin_warp.cuh"
 
@@ -43,6 +44,7 @@ template <typename R> struct TwinSceneOf<R, 2> { using type = TowerScene<R>; };
 
 constexpr int kMaxAlThreads = 512;  // 60 waypoint tiles + the aux warp; <= 128 registers
 constexpr int kXS = 8;  // row stride of x / g / unit in shared memory ([w][joint])
+constexpr int kAlItems = 3;  // sphere items per tile lane (arm + held spheres of a waypoint <= 24)
 
 struct AlLayout {
   int W, NW, nthreads, nwarps, J, B, T, S, SB, NB;
@@ -139,6 +141,7 @@ __device__ __forceinline__ void bar_placed_arrive(int count) {
 }
 __device__ __forceinline__ void bar_placed_sync(int count) { asm volatile("bar.sync 2, %0;" ::"r"(count) : "memory"); }
 
+
 template <typename R>
 struct AlCtx {
   AlProf prof;
@@ -198,11 +201,70 @@ __device__ __forceinline__ R pen_term(R dx, R dy, R dz, R rsum, bool quad, R* sl
   }
 }
 
+// fp32: the same, two obstacles per packed FADD2 / FMUL2 / FFMA2 (one MUFU.RSQ per
+// obstacle); an odd tail is paired with a dummy at the sphere centre (d2 = 0: inactive).
+struct PenAcc2 {
+  F2 v, gx, gy, gz;
+};
+__device__ __forceinline__ PenAcc2 pen_two(PenAcc2 a, F2 cx, F2 cy, F2 cz, float r, bool quad, float ax, float ay,
+                                           float az, float ar, float bx, float by, float bz, float br) {
+  const F2 dx = f2_sub(cx, f2_make(ax, bx)), dy = f2_sub(cy, f2_make(ay, by)), dz = f2_sub(cz, f2_make(az, bz));
+  const F2 d2 = f2_fma(dz, dz, f2_fma(dy, dy, f2_mul(dx, dx)));
+  float d2a, d2b;
+  f2_split(d2, d2a, d2b);
+  const float ia = rsqrtf(d2a), ib = rsqrtf(d2b);
+  const F2 pen = f2_sub(f2_make(r + ar, r + br), f2_mul(d2, f2_make(ia, ib)));
+  float pa, pb;
+  f2_split(pen, pa, pb);
+  const bool la = pa > 0.f, lb = pb > 0.f;  // NaN (d2 = 0) -> inactive
+  pa = la ? pa : 0.f;
+  pb = lb ? pb : 0.f;
+  const float sa = la ? (quad ? 2.f * pa * ia : ia) : 0.f, sb = lb ? (quad ? 2.f * pb * ib : ib) : 0.f;
+  const F2 P = f2_make(pa, pb), SL = f2_make(-sa, -sb);
+  a.v = quad ? f2_fma(P, P, a.v) : f2_add(a.v, P);
+  a.gx = f2_fma(SL, dx, a.gx);
+  a.gy = f2_fma(SL, dy, a.gy);
+  a.gz = f2_fma(SL, dz, a.gz);
+  return a;
+}
+
+__device__ __forceinline__ float pens_fixed_all_f2(const TrajScene<float>& sc, const float* c, float r, int f0,
+                                                   int f1, bool quad, float* g) {
+  const F2 cx = f2_dup(c[0]), cy = f2_dup(c[1]), cz = f2_dup(c[2]);
+  PenAcc2 a;
+  a.v = a.gx = a.gy = a.gz = f2_dup(0.f);
+  const int ns = sc.n_static;
+  int o = 0;
+#pragma unroll 2
+  for (; o + 1 < ns; o += 2)
+    a = pen_two(a, cx, cy, cz, r, quad, sc.st_c[o][0], sc.st_c[o][1], sc.st_c[o][2], sc.st_r[o], sc.st_c[o + 1][0],
+                sc.st_c[o + 1][1], sc.st_c[o + 1][2], sc.st_r[o + 1]);
+  if (o < ns)
+    a = pen_two(a, cx, cy, cz, r, quad, sc.st_c[o][0], sc.st_c[o][1], sc.st_c[o][2], sc.st_r[o], c[0], c[1], c[2],
+                0.f);
+  for (o = f0; o + 1 < f1; o += 2)
+    a = pen_two(a, cx, cy, cz, r, quad, sc.staged[o][0], sc.staged[o][1], sc.staged[o][2], sc.br[o],
+                sc.staged[o + 1][0], sc.staged[o + 1][1], sc.staged[o + 1][2], sc.br[o + 1]);
+  if (o < f1)
+    a = pen_two(a, cx, cy, cz, r, quad, sc.staged[o][0], sc.staged[o][1], sc.staged[o][2], sc.br[o], c[0], c[1], c[2],
+                0.f);
+  float v0, v1, x0, x1, y0, y1, z0, z1;
+  f2_split(a.v, v0, v1);
+  f2_split(a.gx, x0, x1);
+  f2_split(a.gy, y0, y1);
+  f2_split(a.gz, z0, z1);
+  g[0] += x0 + x1;
+  g[1] += y0 + y1;
+  g[2] += z0 + z1;
+  return v0 + v1;
+}
+
 // One sphere against every fixed obstacle (statics, then staged spheres [f0, f1)), on one
 // lane: returns the summed value and adds the unscaled gradient to g.
 template <typename R>
 __device__ __forceinline__ R pens_fixed_all(const TrajScene<R>& sc, const R* c, R r, int f0, int f1, bool quad,
                                             R* g) {
+  if constexpr (sizeof(R) == 4) return pens_fixed_all_f2(sc, c, r, f0, f1, quad, g);
   const R cx = c[0], cy = c[1], cz = c[2];
   R v = R(0), gx = R(0), gy = R(0), gz = R(0);
 #pragma unroll 4
@@ -243,7 +305,7 @@ struct WpState {
 // place; otherwise (want_grad) the gradient is left in g[w*8 + k]. Ends with a barrier.
 // ---------------------------------------------------------------------------------------
 template <typename R, int KIND, int SPB>
-__device__ void al_eval(AlCtx<R>& C, const typename TwinSceneOf<R, KIND>::type& tw, const AlParams& prm, bool quad,
+__device__ __forceinline__ void al_eval(AlCtx<R>& C, const typename TwinSceneOf<R, KIND>::type& tw, const AlParams& prm, bool quad,
                         bool pquad, bool want_grad, R lr) {
   const TrajScene<R>& sc = *C.sc;
   const ChainDesc<R>& ch = sc.ch;
@@ -428,51 +490,59 @@ __device__ void al_eval(AlCtx<R>& C, const typename TwinSceneOf<R, KIND>::type& 
     // ---- P3: placed blocks, placed-pose partials, J^T products
     st.garm = R(0);
     st.gblk = R(0);
-    if (manip) {
-      // uniform trip count over the warp (blocks jb < B - 1; a waypoint of segment b uses
-      // jb < b) so the partial sums below can use the warp-mask shuffles
+    if (manip && B > 1) {
+      // Sphere-major like P2: the lane's items (arm spheres, then held-block spheres; item
+      // it = j + 8k) against the placed spheres of every earlier block. The items' gradients
+      // accumulate in registers and join their P2 slots (written by this same lane) once at
+      // the end; the per-block placed-pose partials are tile reduce-scattered per block.
+      // Uniform trip count over the warp (blocks jb < B - 1; segment b uses jb < b) so the
+      // reduce-scatter can use the warp-mask shuffles.
+      const int n_items = is_wp ? S + (interior ? nh : 0) : 0;
+      R gi[kAlItems][3];
+#pragma unroll
+      for (int k = 0; k < kAlItems; ++k) gi[k][0] = gi[k][1] = gi[k][2] = R(0);
       for (int jb = 0; jb + 1 < B; ++jb) {
         const bool act = is_wp && jb < b;
-        const R cj = C.cp[jb], sj = C.sp[jb];
         R A[4] = {R(0), R(0), R(0), R(0)}, H[4] = {R(0), R(0), R(0), R(0)};
-        for (int q = act ? sc.blk_start[jb] : 0; q < (act ? sc.blk_start[jb + 1] : 0); ++q) {
-          const R px = C.pl[3 * q], py = C.pl[3 * q + 1], pz = C.pl[3 * q + 2], rq = sc.br[q];
-          const R drx = -sj * sc.bu[q][0] - cj * sc.bu[q][1];
-          const R dry = cj * sc.bu[q][0] - sj * sc.bu[q][1];
-          if (j < J) {
-            for (int s = ch.link_start[j]; s < ch.link_start[j + 1]; ++s) {
-              const R* a = C.armw + (w * S + s) * 3;
-              const R dx = a[0] - px, dy = a[1] - py, dz = a[2] - pz;
+        if (act) {
+          const R cj = C.cp[jb], sj = C.sp[jb];
+          const int q0 = sc.blk_start[jb], q1 = sc.blk_start[jb + 1];
+#pragma unroll
+          for (int k = 0; k < kAlItems; ++k) {
+            const int it = j + kTile * k;
+            if (it >= n_items) break;
+            const bool arm = it < S;
+            const int si = arm ? it : it - S;
+            const R* c = arm ? C.armw + (w * S + si) * 3 : C.hp + (w * SBn + si) * 3;
+            const R cx = c[0], cy = c[1], cz = c[2];
+            const R rr = arm ? ch.arm_r[si] : sc.br[h0 + si];
+            R v = R(0), ax = R(0), ay = R(0), az = R(0), aw = R(0);
+            for (int q = q0; q < q1; ++q) {
+              const R dx = cx - C.pl[3 * q], dy = cy - C.pl[3 * q + 1], dz = cz - C.pl[3 * q + 2];
               R sl;
-              carm += pen_term(dx, dy, dz, ch.arm_r[s] + rq, quad, &sl);
-              if (want_grad && sl != R(0)) {
-                R* ga = C.ga + (w * S + s) * 3;
-                ga[0] -= sl * dx;
-                ga[1] -= sl * dy;
-                ga[2] -= sl * dz;
-                A[0] += sl * dx;
-                A[1] += sl * dy;
-                A[2] += sl * dz;
-                A[3] += (sl * dx) * drx + (sl * dy) * dry;
-              }
+              v += pen_term(dx, dy, dz, rr + sc.br[q], quad, &sl);
+              const R fx = sl * dx, fy = sl * dy, fz = sl * dz;
+              ax += fx;
+              ay += fy;
+              az += fz;
+              // d(block sphere q)/d(placed yaw) (trajopt.py:601-635)
+              aw += fx * (-sj * sc.bu[q][0] - cj * sc.bu[q][1]) + fy * (cj * sc.bu[q][0] - sj * sc.bu[q][1]);
             }
-          }
-          if (interior) {
-            for (int s = j; s < nh; s += kTile) {
-              const R* h = C.hp + (w * SBn + s) * 3;
-              const R dx = h[0] - px, dy = h[1] - py, dz = h[2] - pz;
-              R sl;
-              cblk += pen_term(dx, dy, dz, sc.br[h0 + s] + rq, quad, &sl);
-              if (want_grad && sl != R(0)) {
-                R* gh = C.gh + (w * SBn + s) * 3;
-                gh[0] -= sl * dx;
-                gh[1] -= sl * dy;
-                gh[2] -= sl * dz;
-                H[0] += sl * dx;
-                H[1] += sl * dy;
-                H[2] += sl * dz;
-                H[3] += (sl * dx) * drx + (sl * dy) * dry;
-              }
+            gi[k][0] -= ax;
+            gi[k][1] -= ay;
+            gi[k][2] -= az;
+            if (arm) {
+              A[0] += ax;
+              A[1] += ay;
+              A[2] += az;
+              A[3] += aw;
+              carm += v;
+            } else {
+              H[0] += ax;
+              H[1] += ay;
+              H[2] += az;
+              H[3] += aw;
+              cblk += v;
             }
           }
         }
@@ -482,7 +552,19 @@ __device__ void al_eval(AlCtx<R>& C, const typename TwinSceneOf<R, KIND>::type& 
           if (act) C.pg[((w * 2 + (j >> 2)) * B + jb) * 4 + (j & 3)] = r;
         }
       }
+      if (want_grad) {
+#pragma unroll
+        for (int k = 0; k < kAlItems; ++k) {
+          const int it = j + kTile * k;
+          if (it >= n_items) break;
+          R* go = it < S ? C.ga + (w * S + it) * 3 : C.gh + (w * SBn + it - S) * 3;
+          go[0] += gi[k][0];
+          go[1] += gi[k][1];
+          go[2] += gi[k][2];
+        }
+      }
     }
+    __syncwarp();  // the J^T products below read sphere gradients other lanes of the tile own
     if (want_grad) {
       // arm: suffix sums over links >= k of (g, a x g), lane k = joint k (trajopt.py:586-590)
       R G[3] = {R(0), R(0), R(0)}, Mv[3] = {R(0), R(0), R(0)};
@@ -563,6 +645,7 @@ __device__ void al_eval(AlCtx<R>& C, const typename TwinSceneOf<R, KIND>::type& 
   R s_pl = R(0), s_arm = R(0), s_blk = R(0);
   if (tid == 0 || grad_lane) {
     R o = R(0), ca = R(0), cb = R(0);
+#pragma unroll 4
     for (int wi = 0; wi < C.L.NW / 32; ++wi) {
       o += C.red[4 * wi];
       ca += C.red[4 * wi + 1];
@@ -592,9 +675,14 @@ __device__ void al_eval(AlCtx<R>& C, const typename TwinSceneOf<R, KIND>::type& 
   // waypoint order, by its final-waypoint tile: lane j forms item j ([class j/4][xyz|yaw])
   if (want_grad && manip && is_wp && t == T - 1) {
     const int cls = j >> 2, i = j & 3;
-    R sum = R(0);
-    for (int wv = (b + 1) * T; wv < W; ++wv) sum += C.pg[((wv * 2 + cls) * B + b) * 4 + i];
-    C.pgsum[(cls * B + b) * 4 + i] = sum;
+    R s0 = R(0), s1 = R(0);  // two interleaved partial sums (fixed order)
+    int wv = (b + 1) * T;
+    for (; wv + 1 < W; wv += 2) {
+      s0 += C.pg[((wv * 2 + cls) * B + b) * 4 + i];
+      s1 += C.pg[(((wv + 1) * 2 + cls) * B + b) * 4 + i];
+    }
+    if (wv < W) s0 += C.pg[((wv * 2 + cls) * B + b) * 4 + i];
+    C.pgsum[(cls * B + b) * 4 + i] = s0 + s1;
     __syncwarp(tl.mask);
   }
 
@@ -656,7 +744,7 @@ __device__ void al_eval(AlCtx<R>& C, const typename TwinSceneOf<R, KIND>::type& 
 // current x (a preceding al_eval). Leaves the max violation in scal[kWorst].
 // ---------------------------------------------------------------------------------------
 template <typename R, int KIND, int SPB>
-__device__ void al_validate(AlCtx<R>& C, const typename TwinSceneOf<R, KIND>::type& tw, const AlParams& prm) {
+__device__ __forceinline__ void al_validate(AlCtx<R>& C, const typename TwinSceneOf<R, KIND>::type& tw, const AlParams& prm) {
   const TrajScene<R>& sc = *C.sc;
   const ChainDesc<R>& ch = sc.ch;
   const int tid = threadIdx.x;
@@ -886,8 +974,10 @@ struct AlRecords {
   const int32_t* n_active;                   // device count of live particles (nullptr = gridDim.x)
 };
 
-template <typename R, int KIND, int SPB>
-__global__ void __launch_bounds__(kMaxAlThreads) k_solve_al(const TrajScene<R>* __restrict__ g_scene,
+// MAXT: the block-size bound. 256 (C2-sized particles, <= 28 waypoints) lets ptxas keep the
+// whole tower engine in up to 255 registers; 512 caps it at 128 (launch_solve_al picks).
+template <typename R, int KIND, int SPB, int MAXT = kMaxAlThreads>
+__global__ void __launch_bounds__(MAXT, 1) k_solve_al(const TrajScene<R>* __restrict__ g_scene,
                                                             const typename TwinSceneOf<R, KIND>::type tw, AlLayout L,
                                                             AlParams prm, const R* __restrict__ values, int P,
                                                             AlRecords rec) {

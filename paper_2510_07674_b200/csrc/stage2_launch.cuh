@@ -24,6 +24,7 @@ inline int al_layout_for(const Traj& tr, int T, AlLayout* L) {
   *L = al_layout<R>(tr.B, T, tr.J, tr.S, tr.SB, tr.NB);
   SPASM_REQUIRE(T >= 2, "segments need at least two waypoints");
   SPASM_REQUIRE(L->nthreads <= kMaxAlThreads, "too many waypoints per particle (B*T must be <= 60)");
+  SPASM_REQUIRE(tr.S + tr.SB <= kTile * kAlItems, "arm spheres + spheres of one block must be <= 24");
   SPASM_REQUIRE(L->total <= 227 * 1024, "trajectory particle does not fit in shared memory");
   return SPASM_OK;
 }
@@ -139,6 +140,9 @@ int launch_solve_al(const Traj& tr, const AlParams& prm, const R* values, int64_
     st = dispatch_twin<R>(tr, [&](auto kind, const auto& tw) -> int {
       constexpr int K = decltype(kind)::value;
       auto kern = k_solve_al<R, K, 0>;
+      if constexpr (sizeof(R) == 4) {
+        if (L.nthreads <= 256) kern = k_solve_al<R, K, 0, 256>;  // room for more registers per thread
+      }
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L.total);
       kern<<<(unsigned)P, L.nthreads, L.total, s>>>(tr.dev<R>(), tw, L, prm, values, (int)P, rec);
       SPASM_CHECK_LAUNCH();
