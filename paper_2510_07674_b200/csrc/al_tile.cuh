@@ -464,6 +464,7 @@ __device__ __forceinline__ void al_eval(AlCtx<R>& C, const typename TwinSceneOf<
         obj_w += w_start * ((((st.d0[0] * st.d0[0] + st.d0[1] * st.d0[1]) + st.d0[2] * st.d0[2]) + th * th) +
                             st.dy0 * st.dy0);
     }
+    C.prof.arrive(5, C.L.NW);  // sub-mark: leg + start terms done
     // Sphere-major: the tile's 8 lanes take the waypoint's spheres (arm spheres, then the
     // held-block spheres) round-robin, each against the whole fixed list, so a sphere's
     // gradient stays lane-local (no tile sums) and the values join the warp sums below.
@@ -686,6 +687,7 @@ __device__ __forceinline__ void al_eval(AlCtx<R>& C, const typename TwinSceneOf<
     __syncwarp(tl.mask);
   }
 
+  C.prof.arrive(7, C.L.NW);  // sub-mark: totals + placed partial sums done
   // gradient assembly (lane k = joint k) + optional update
   if (grad_lane) {
     R gq = R(0);

@@ -33,4 +33,6 @@ for k, n in names.items():
     if k < 5:
         line += f"   own work: tile t0 {out[12 + k] / max(1, outers):12.0f}  aux {out[20 + k] / max(1, outers):12.0f}"
     print(line)
+print(f"  tile t0 sub-marks: leg+start done at {out[17] / max(1, outers):.0f}, B totals+pgsum done at "
+      f"{out[19] / max(1, outers):.0f} cycles/outer (since the phase's start)")
 print(f"  aux P2 split: placed poses done at {out[25] / max(1, outers):.0f}, twin done at {out[26] / max(1, outers):.0f} cycles/outer")
