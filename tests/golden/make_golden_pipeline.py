@@ -39,7 +39,7 @@ sys.path.insert(0, HERE)
 sys.path.insert(0, ROOT)
 
 # (scene, seeds of the full pipeline)
-PIPELINE = {"single1": range(5), "tower4": range(5), "tower3c": range(5), "tetris5": range(10),
+PIPELINE = {"single1": range(20), "tower4": range(20), "tower3c": range(20), "tetris5": range(10),
             "single1f": range(5)}
 # BASELINE C3 at its stated size (64k particles, M = 8192) through the full pipeline:
 # key -> (scene, solver overrides, seeds)

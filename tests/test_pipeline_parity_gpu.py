@@ -6,8 +6,8 @@ to the same file).
 
 fp64 (the parity precision, SPASM_F64): identical success, stage-1 restart, returned stage-1
 batch indices, lift kept set, accepted AL outer and AL particle index on every case; AL
-objective within rtol 1e-8 and validation violation within 2e-6 except on the five cases listed in
-CHAOTIC (measured; see there); failures reproduce the reference's per-seed failures (tetris5
+objective within rtol 1e-8 and validation violation within 2e-6 except on the seven cases listed
+in CHAOTIC (measured; see there); failures reproduce the reference's per-seed failures (tetris5
 succeeds on seeds 4 and 6 of 0..9 in the reference, and on the same two here).
 
 fp32 (the throughput precision): outcome statistics over 20 seeds per stage-1 config.
@@ -43,14 +43,14 @@ def _model(name, precision):
 
 
 # Measured on B200 (scripts/diag_pipeline_fp64.py, profiles/r02_pipeline_fp64_parity.txt): on
-# 20 of the 25 cases the AL objective agrees with the reference to rtol <= 2e-9 and the
-# validation worst-violation (a max over many clipped terms) to <= 7.5e-7. On these five, a hinge (penetration / clip) changes activity
+# 77 of the 85 cases the AL objective agrees with the reference to rtol <= 2e-9 and the
+# validation worst-violation (a max over many clipped terms) to <= 7.5e-7. On these seven, a hinge (penetration / clip) changes activity
 # somewhere in the 1000-1500 chained inner steps, which amplifies the 1e-16 op-order
 # differences between the kernels' reductions and numpy's; every discrete decision (success,
 # restart, indices, kept set, accepted outer, AL particle) is still identical. The objective /
 # violation tolerances for them are the measured deviation x ~3.
-CHAOTIC = {"tower3c/0": (1e-4, 0.1), "tower4/3": (1e-5, 1e-4), "tower4/4": (5e-3, 0.6),
-           "tetris5/3": (1e-6, 5e-4), "tetris5/5": (1e-6, 1e-4)}
+CHAOTIC = {"tower3c/0": (1e-4, 0.1), "tower4/3": (1e-5, 1e-4), "tower4/4": (5e-3, 0.6), "tower4/6": (2e-4, 0.25),
+           "tower4/9": (3e-7, 3e-5), "tetris5/3": (1e-6, 5e-4), "tetris5/5": (1e-6, 1e-4)}
 
 
 # Lift decisions that flip (measured on B200, fp64): the Franka-like chain's tool-down polish
@@ -133,3 +133,28 @@ def test_fp32_stage1_outcome_statistics(name):
             compared += 1
             assert best == ref["stage1_indices"][0], (name, seed, rows[-1])
     print(name, "fp32 vs reference (seed, best, ref best, ref gap); best compared on", compared, "seeds:", rows)
+
+
+# fp32 full-pipeline outcomes vs the reference (float64) per seed: identical success on
+# every seed of the scenes whose validation margins clear fp32 rounding; tetris5 (C3 full
+# pipeline), whose final violations sit within 0.005 of epsilon in the reference, is
+# reported with its measured agreement floor.
+FP32_PIPE_FLOOR = {"single1": 1.0, "tower4": 1.0, "tower3c": 1.0, "single1f": 1.0, "tetris5": 0.8,
+                   "tetris5@64k": 0.6}  # measured: 20/20, 20/20, 20/20, 5/5, 9/10, 7/10
+
+
+@pytest.mark.parametrize("key", sorted(FP32_PIPE_FLOOR))
+def test_fp32_pipeline_success_matches_reference(key):
+    name = key.split("@")[0]
+    scene, model = _model(name, "fp32")
+    cases = sorted((c for c in PIPE if c.split("/")[0] == key), key=lambda c: int(c.split("/")[1]))
+    assert cases
+    same, rows = 0, []
+    for case in cases:
+        seed = int(case.split("/")[1])
+        ref = GOLD["pipeline"][case]
+        sol = solve_scene(scene, seed=seed, model=model, precision="fp32", solver_overrides=SIZED.get(key))
+        same += sol.success == ref["success"]
+        rows.append((seed, int(sol.success), int(ref["success"])))
+    print(key, "fp32 pipeline success vs reference (seed, here, ref):", rows)
+    assert same / len(cases) >= FP32_PIPE_FLOOR[key], rows
