@@ -72,6 +72,14 @@ struct Tile {
   // shuffles need no divergence handling)
   __device__ __forceinline__ bool all(bool p) const { return __all_sync(mask, p); }
   __device__ __forceinline__ bool any(bool p) const { return __any_sync(mask, p); }
+  // max over the tile of a NON-NEGATIVE value: fp32 takes one REDUX.MAX on the bit patterns
+  // (non-negative IEEE floats order like their bits; 22 cycles against 3 shuffle levels),
+  // fp64 the shuffle tree
+  template <typename R>
+  __device__ __forceinline__ R max_nonneg(R v) const {
+    if constexpr (sizeof(R) == 4) return __uint_as_float(__reduce_max_sync(mask, __float_as_uint(v)));
+    else return max(v);
+  }
   template <typename R>
   __device__ __forceinline__ R max(R v) const {
     v = fmax(v, xr(v, 1));
@@ -247,7 +255,7 @@ __device__ __forceinline__ R tile_dls(const Tile& tl, const R (&col)[NR], const 
   R dq = R(0);
 #pragma unroll
   for (int a = 0; a < NR; ++a) dq += col[a] * y[a];
-  const R mx = tl.max(fabs(dq));
+  const R mx = tl.max_nonneg(fabs(dq));
   return dq * fmin(R(1), R(0.5) / fmax(mx, R(1e-12)));
 }
 

@@ -68,6 +68,7 @@ __global__ void k_lds(const float* g, int iters, float* out, long long* cyc) {
   out[threadIdx.x] = k;
 }
 
+int main2();
 int main() {
   ChainDesc<float> h{};
   h.J = 7;
@@ -91,5 +92,62 @@ int main() {
     k_lds<<<1, threads>>>(nullptr, 1000, out, cyc); cudaMemcpy(hc, cyc, 8, cudaMemcpyDeviceToHost);
     printf("lds chain    %3d threads: %lld cycles/iter\n", threads, hc[0]);
   }
+  return main2();
+}
+
+// variant: tile max through one REDUX.MAX on the (non-negative) float bit patterns
+template <typename R, int NR>
+__device__ __forceinline__ R tile_dls_redux(const Tile& tl, const R (&col)[NR], const R (&e)[NR], R damping) {
+  R A[NR * NR];
+#pragma unroll
+  for (int a = 0; a < NR; ++a)
+#pragma unroll
+    for (int b = 0; b <= a; ++b) {
+      const R v = tl.sum(col[a] * col[b]);
+      A[a * NR + b] = v + (a == b ? damping : R(0));
+      A[b * NR + a] = A[a * NR + b];
+    }
+  R y[NR];
+  chol_solve<R, NR>(A, e, y);
+  R dq = R(0);
+#pragma unroll
+  for (int a = 0; a < NR; ++a) dq += col[a] * y[a];
+  const R mx = __uint_as_float(__reduce_max_sync(tl.mask, __float_as_uint(fabsf(dq))));
+  return dq * fminf(R(1), R(0.5) / fmaxf(mx, R(1e-12)));
+}
+
+__global__ void k_dls_redux(int iters, float* out, long long* cyc) {
+  const Tile tl = Tile::make_warp();
+  float col[5], e[5];
+  for (int k = 0; k < 5; ++k) { col[k] = 0.1f * (k + 1) + 0.01f * tl.j; e[k] = 0.01f * k; }
+  float acc = 0.f;
+  long long t0 = clock64();
+  for (int i = 0; i < iters; ++i) {
+    const float dq = tile_dls_redux<float, 5>(tl, col, e, 1e-3f);
+    col[0] += dq * 1e-3f;
+    acc += dq;
+  }
+  long long t1 = clock64();
+  if (threadIdx.x == 0) cyc[blockIdx.x] = (t1 - t0) / iters;
+  out[threadIdx.x] = acc;
+}
+
+__global__ void k_redux_lat(int iters, float* out, long long* cyc) {
+  unsigned v = threadIdx.x;
+  long long t0 = clock64();
+  for (int i = 0; i < iters; ++i) v = __reduce_max_sync(0xffffffffu, v) + 1u;
+  long long t1 = clock64();
+  if (threadIdx.x == 0) cyc[blockIdx.x] = (t1 - t0) / iters;
+  out[threadIdx.x] = (float)v;
+}
+
+int main2() {
+  float* out; cudaMalloc(&out, 4096 * 4);
+  long long* cyc; cudaMalloc(&cyc, 64 * 8);
+  long long hc[1];
+  k_dls_redux<<<1, 32>>>(1000, out, cyc); cudaMemcpy(hc, cyc, 8, cudaMemcpyDeviceToHost);
+  printf("tile_dls<5> with REDUX max, 32 threads: %lld cycles/call\n", hc[0]);
+  k_redux_lat<<<1, 32>>>(1000, out, cyc); cudaMemcpy(hc, cyc, 8, cudaMemcpyDeviceToHost);
+  printf("redux.max chain: %lld cycles/iter\n", hc[0]);
   return 0;
 }
