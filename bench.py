@@ -598,8 +598,13 @@ def run_reference(args):
         return
     from paper_2510_07674_b200.problems import load_scene
 
+    from paper_2510_07674_b200.bench_api import _solver_config as _sc
+
     scene_name, over, stage1_only, desc = WORKLOADS[args.workload]
     scene = load_scene(scene_name)
+    if world > 1:  # the b200 arm's weak-scaled workload: world x the per-GPU (n, m) per restart
+        b0 = _sc(scene, 0, over, False)
+        over = {**over, "n": b0.n * world, "m": b0.m * world}
     threads = os.cpu_count() or 1
     mr = 1 if stage1_only else None
     kind = _reference_impl()
