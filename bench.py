@@ -407,6 +407,10 @@ def run_b200(args, workload=None, sub=False):
         # reference bench.solve_scene span: stage 1 (+ lift + AL), excluding scene load and the
         # final independent validate (bench.py:190-247); p50_step_ms is the whole timed step
         "p50_solve_ms": statistics.median(s.time_ms for s in sols),
+        # the metric's "at 100 % success": p50 over the successful solves (differs when the
+        # workload's scene is not always solvable, e.g. C3p, where the reference fails too)
+        "p50_solve_ms_successes": (statistics.median(s.time_ms for s in sols if s.success)
+                                   if any(s.success for s in sols) else None),
         "p50_step_ms": statistics.median(wall_ms),
         "success_rate": succ / steps,
         "higher_is_better": True,
@@ -663,8 +667,9 @@ def main():
         line["sub_records"] = {}
         for w in ("c5", "c3", "c1", "c1f"):
             sub = run_b200(args, workload=w, sub=True)
-            keep = ("value", "unit", "ms_per_step", "p50_solve_ms", "p50_step_ms", "success_rate", "steps", "warmup",
-                    "config", "e2e", "roofline", "clocks", "gpu_launches", "breakdown", "reference_outcomes")
+            keep = ("value", "unit", "ms_per_step", "p50_solve_ms", "p50_solve_ms_successes", "p50_step_ms",
+                    "success_rate", "steps", "warmup", "config", "e2e", "roofline", "clocks", "gpu_launches",
+                    "breakdown", "reference_outcomes")
             line["sub_records"][w] = {k: sub[k] for k in keep if k in sub}
     if args.gpus == 1 and dist_env()[1] == 1 and args.workload == "c3p" and not args.no_sub:
         # C3's 4- and 6-object variants (stage 1 at 64k) beside the 5-object full pipeline
