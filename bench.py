@@ -676,7 +676,7 @@ def main():
         line["sub_records"] = {}
         for w in ("c3_4", "c3_6"):
             sub = run_b200(args, workload=w, sub=True)
-            keep = ("value", "unit", "ms_per_step", "p50_solve_ms", "p50_step_ms", "success_rate", "steps", "warmup",
+            keep = ("value", "unit", "ms_per_step", "p50_solve_ms", "p50_solve_ms_successes", "p50_step_ms", "success_rate", "steps", "warmup",
                     "config", "e2e", "roofline", "clocks", "gpu_launches", "breakdown")
             line["sub_records"][w] = {k: sub[k] for k in keep if k in sub}
     print(json.dumps(line))
