@@ -573,9 +573,10 @@ class PendingSolve:
     ``collect``. ``device_rows`` exposes the compacted result rows in device memory, so a
     stage-2 consumer can read them in stream order without a round trip."""
 
-    def __init__(self, model, config, t0, warm):
+    def __init__(self, model, config, t0, warm, workspace):
         self.model, self.config, self.t0 = model, config, t0
         self._warm = warm  # kept alive until the launch has copied it
+        self._ws = workspace  # the device rows live in it: kept alive until collect (cache eviction)
 
     def device_rows(self):
         """(rows pointer: float64 (p_return, D), count pointer: int32) on the device."""
@@ -593,6 +594,7 @@ class PendingSolve:
         rep = nat.spasm_solve_report()
         status = nat.check(nat.load().spasm_solve_collect(self.model.handle, nat.ptr(parts), nat.ptr(costs),
                                                           nat.ptr(idx), ctypes_byref(rep)), "solve_collect")
+        self._ws = None
         return _result(status, rep, parts, costs, idx, self.t0, None)
 
 
@@ -626,7 +628,7 @@ def solve_launch(model: NativeCostModel, config: OptimizerConfig, *, warm_seeds=
     ws = _WS.get(model, cfg, n_warm)
     nat.check(nat.load().spasm_solve_launch(model.handle, model.dtype_id, ctypes_byref(cfg), nat.ptr(warm), n_warm,
                                             nat.ptr(ws), ws.numel(), nat.stream_handle()), "solve_launch")
-    return PendingSolve(model, config, t0, warm)
+    return PendingSolve(model, config, t0, warm, ws)
 
 
 def _solve_native(model: NativeCostModel, config: OptimizerConfig, warm_seeds, trace: bool, sampler: int):

@@ -219,7 +219,8 @@ def topm_exchange(ops, comm, restart: int, row_lo: int, n_local: int, m: int):
         h = comm.all_reduce_sum(ops.topm_hist(st))
         ops.topm_pick(st, h)
     take = allot_top_m(comm.all_gather(ops.topm_local(st)).cpu().numpy())
-    assert int(take.sum()) == m, (take, m)
+    if int(take.sum()) != m:  # the ranks disagree on the threshold: a broken exchange, not a result
+        raise RuntimeError(f"top-m select allotted {int(take.sum())} records for m = {m}: {take.tolist()}")
     cap = max(1, int(take.max()))
     return comm.all_gather(ops.topm_contrib(int(take[comm.rank]), cap)).reshape(comm.world, cap, 2)
 
