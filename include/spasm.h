@@ -301,6 +301,12 @@ typedef struct {
   double objective;               /* AlResult.objective */
   double least_violation;         /* TrajOptFailure.best_violation */
   double device_ms;
+  /* float64 validate (trajopt.py:1071-1153) of the accepted trajectory, run on the device in
+   * the same stream before the one host sync (the independent re-check of bench.py:249);
+   * meaningful when status == SPASM_OK */
+  double checked_violation;
+  int32_t checked_feasible;
+  int32_t reserved;
 } spasm_al_result;
 
 /* fk_batch (+ yaw_jacobian_batch) (robot.py:160-224). Q (n,dof) device; ee (n,3), rot (n,9);

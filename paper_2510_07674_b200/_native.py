@@ -136,6 +136,9 @@ class spasm_al_result(ctypes.Structure):
         ("objective", c_double),
         ("least_violation", c_double),
         ("device_ms", c_double),
+        ("checked_violation", c_double),
+        ("checked_feasible", c_int32),
+        ("reserved", c_int32),
     ]
 
 

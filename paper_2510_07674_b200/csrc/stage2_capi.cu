@@ -142,8 +142,13 @@ static AlParams al_params(const spasm_al_config& c) {
 
 static size_t al_up(size_t x) { return (x + 255) & ~(size_t)255; }
 
+__global__ void k_widen(const float* __restrict__ in, int64_t n, double* __restrict__ out) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = (double)in[i];
+}
+
 struct AlWs {
-  size_t mu, lam, cons, upd, obj, viol, feas, first, nout, kstar, res, best, total;
+  size_t mu, lam, cons, upd, obj, viol, feas, first, nout, kstar, res, best, best64, total;
 };
 
 static AlWs al_ws_layout(const Traj& tr, int dtype, int64_t P, const spasm_al_config& c) {
@@ -168,6 +173,7 @@ static AlWs al_ws_layout(const Traj& tr, int dtype, int64_t P, const spasm_al_co
   L.kstar = take(16);
   L.res = take(sizeof(AlResultBlock));
   L.best = take((size_t)std::max<int64_t>(P, 1) * tr.B * c.waypoints * tr.J * r);
+  L.best64 = take((size_t)tr.B * c.waypoints * tr.J * 8);  // the accepted trajectory in float64
   L.total = off;
   return L;
 }
@@ -524,9 +530,26 @@ int spasm_solve_al(const spasm_traj* t, int dtype, const spasm_al_config* cfg, c
   else
     st = launch_solve_al<double>(*t, prm, (const double*)values, P, rec, lift_status, (double*)best_values, res_dev,
                                  s);
+  if (st == SPASM_OK && best_values) {
+    // the float64 re-check of the accepted trajectory, queued behind the solve (its result
+    // joins the one D2H copy below); on failure best_values holds no trajectory and the
+    // check is ignored
+    const int64_t nv = (int64_t)t->B * cfg->waypoints * t->J;
+    double* best64 = reinterpret_cast<double*>(reinterpret_cast<char*>(ws) + L.best64);
+    if (dtype == SPASM_F32) {
+      k_widen<<<ceil_div(nv, 256), 256, 0, s>>>((const float*)best_values, nv, best64);
+      if (cudaGetLastError() != cudaSuccess) st = SPASM_ERR_CUDA;
+    } else {
+      if (cudaMemcpyAsync(best64, best_values, (size_t)nv * 8, cudaMemcpyDeviceToDevice, s) != cudaSuccess)
+        st = SPASM_ERR_CUDA;
+    }
+    if (st == SPASM_OK)
+      st = launch_validate<double>(*t, prm, best64, 1, &res_dev->check_feasible, &res_dev->check_violation, s);
+  }
   if (st) {
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
+    if (st == SPASM_ERR_CUDA) set_last_error("spasm_solve_al: re-check launch failed");
     return st;
   }
   cudaEventRecord(e1, s);
@@ -550,6 +573,9 @@ int spasm_solve_al(const spasm_traj* t, int dtype, const spasm_al_config* cfg, c
   result->objective = host->objective;
   result->least_violation = host->least_violation;
   result->device_ms = ms;
+  result->checked_violation = host->check_violation;
+  result->checked_feasible = host->check_feasible;
+  result->reserved = 0;
   return host->status;
 }
 

@@ -42,6 +42,11 @@ struct AlResultBlock {
   int32_t lift_pick_fail;  // first unreachable staged pose (-1 none)
   double objective;
   double least_violation;
+  // float64 re-check of the accepted trajectory (validate, trajopt.py:1071-1153), run on the
+  // device behind the AL solve: the independent check bench.solve_scene makes (bench.py:249)
+  double check_violation;
+  uint8_t check_feasible;
+  uint8_t pad[7];
 };
 
 }  // namespace spasm

@@ -808,9 +808,9 @@ def solve_stage2(scene, result, config, seed, trajopt_overrides, t0, precision: 
         return SceneSolution(False, time_ms, result.report.restarts, result.report.steps, w, max_violation=w,
                              stats=stats, bookkeeping=book), result
     traj = _particle_trajectory(best.double().cpu().numpy(), geo)
-    feasible, worst = validate(traj, scene.problem, scene.chain, grasp=scene.grasp,
-                               static_centers=scene.obstacle_centers, static_radii=scene.obstacle_radii,
-                               epsilon=tcfg.validation_epsilon, precision="fp64")
+    # the independent float64 validate of the accepted trajectory (bench.py:249) ran on the
+    # device behind the AL solve (spasm_solve_al: checked_feasible / checked_violation)
+    feasible, worst = bool(res.checked_feasible), float(res.checked_violation)
     return SceneSolution(bool(feasible), time_ms, result.report.restarts, result.report.steps, worst,
                          placement=np.asarray(result.particles)[int(kept[res.particle_index])].copy(),
                          trajectory=traj, path_length=trajectory_path_length(traj), max_violation=worst, stats=stats,
@@ -838,6 +838,6 @@ def solve_motion_scene(scene, seed, trajopt_overrides, precision: str = "fp32"):
         w = float(res.least_violation)
         return SceneSolution(False, time_ms, 0, 0, w, max_violation=w, stats=stats)
     traj = _particle_trajectory(best.double().cpu().numpy(), geo)
-    feasible, worst = validate(traj, scene.problem, scene.chain, epsilon=tcfg.validation_epsilon, precision="fp64")
+    feasible, worst = bool(res.checked_feasible), float(res.checked_violation)  # device float64 validate
     return SceneSolution(bool(feasible), time_ms, 0, 0, worst, trajectory=traj,
                          path_length=trajectory_path_length(traj), max_violation=worst, stats=stats)

@@ -210,3 +210,21 @@ def test_solve_scene_motion_corridor3():
 
     sol = solve_scene(load_scene("corridor3"), seed=0, precision="fp64")
     assert sol.success
+
+
+@pytest.mark.parametrize("name,precision", [("tower3c", "fp32"), ("single1", "fp32"), ("tower4", "fp64"),
+                                            ("tetris5", "fp32")])
+def test_device_recheck_equals_validate(name, precision):
+    """solve_scene's independent float64 re-check (bench.py:249) runs on the device behind the
+    AL solve (spasm_solve_al checked_*); it must equal trajopt.validate on the returned
+    trajectory, bit for bit."""
+    from paper_2510_07674_b200.bench_api import solve_scene
+
+    sc = load_scene(name)
+    for seed in (0, 4):
+        sol = solve_scene(sc, seed=seed, precision=precision)
+        if sol.trajectory is None:
+            continue
+        ok, worst = tj.validate(sol.trajectory, sc.problem, sc.chain, grasp=sc.grasp, static_centers=sc.obstacle_centers,
+                                static_radii=sc.obstacle_radii, epsilon=_cfg(sc).validation_epsilon, precision="fp64")
+        assert sol.success == ok and sol.max_violation == worst
