@@ -363,6 +363,10 @@ int spasm_solve_al(const spasm_traj* traj, int dtype, const spasm_al_config* cfg
  * 0 / the aux warp reached each phase's barrier). enable 1/0; out (28 doubles, optional)
  * receives and resets the counters. */
 int spasm_al_profile(int enable, double* out);
+/* Diagnostic: per-warp own-work cycles per phase of the fp32 AL kernel (lane 0 of every
+ * warp; out = 32 x 8 doubles [warp][phase], summed over CTAs) followed by 4 pick-polish
+ * counters (iterations, calls, calls at the cap, max iterations); 260 doubles. Resets. */
+int spasm_al_profile_warps(double* out);
 
 #ifdef __cplusplus
 }

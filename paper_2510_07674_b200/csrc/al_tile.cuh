@@ -110,6 +110,8 @@ enum : int {
 // deltas between consecutive marks; off unless enabled (one predicated branch per mark).
 static __device__ unsigned long long g_al_prof[12];
 static __device__ unsigned long long g_al_arrive[2][8];  // [tile thread 0 | aux lane 0][phase]
+static __device__ unsigned long long g_al_warp[32][8];    // [warp (lane 0)][phase]: own work per warp
+static __device__ unsigned long long g_al_polish[4];      // pick polish: iterations, calls, at the cap, max
 static __device__ int g_al_prof_on;
 struct AlProf {
   bool on = false;
@@ -120,8 +122,11 @@ struct AlProf {
   }
   // before a phase-ending barrier: how long this thread's own work in the phase took
   __device__ __forceinline__ void arrive(int k, int aux_tid) {
-    if (on && (threadIdx.x == 0 || threadIdx.x == aux_tid))
-      atomicAdd(&g_al_arrive[threadIdx.x == 0 ? 0 : 1][k], (unsigned long long)(clock64() - t));
+    if (on && (threadIdx.x & 31) == 0) {
+      const unsigned long long d = (unsigned long long)(clock64() - t);
+      atomicAdd(&g_al_warp[threadIdx.x >> 5][k], d);
+      if (threadIdx.x == 0 || threadIdx.x == aux_tid) atomicAdd(&g_al_arrive[threadIdx.x == 0 ? 0 : 1][k], d);
+    }
   }
   // after the barrier: phase time (slowest warp) as seen by thread 0
   __device__ __forceinline__ void mark(int k) {
@@ -330,9 +335,6 @@ __device__ __forceinline__ void al_eval(AlCtx<R>& C, const typename TwinSceneOf<
   const int bar_count = C.L.NW + 32;
   WpState<R> st;
   R obj_w = R(0), carm = R(0), cblk = R(0);
-  // tower twin helpers (twin_warp.cuh): the last two tile warps take the stability
-  // supports and the cube-obstacle pairs
-  const int twin_ext = KIND == 2 ? (C.L.NW >= 64 ? 2 : 1) : 0;
 
   // warp-role predicates from a warp vote: uniform by construction, so ptxas can branch on
   // them without divergence handling and the warp-wide shuffles inside stay plain SHFLs
@@ -376,7 +378,7 @@ __device__ __forceinline__ void al_eval(AlCtx<R>& C, const typename TwinSceneOf<
       __syncwarp();
       bar_placed_arrive(bar_count);
       if (C.prof.on && lane == 0) atomicAdd(&g_al_arrive[1][5], (unsigned long long)(clock64() - C.prof.t));
-      R cpl = twin_warp<R, KIND, SPB>(tw, C.rows, C.gpose, C.scr, lane, want_grad, pquad, twin_ext);
+      R cpl = twin_warp<R, KIND, SPB>(tw, C.rows, C.gpose, C.scr, lane, want_grad, pquad);
       if (C.prof.on && lane == 0) atomicAdd(&g_al_arrive[1][6], (unsigned long long)(clock64() - C.prof.t));
       if (sc.anchor) {  // yaw anchor (trajopt.py:531-539): lane bb takes segment bb, warp-summed
         R av = R(0);
@@ -432,14 +434,7 @@ __device__ __forceinline__ void al_eval(AlCtx<R>& C, const typename TwinSceneOf<
     else __syncwarp();
     C.prof.mark(0);
 
-    // ---- P2: tower twin helper parts, leg, start terms, fixed obstacles
-    if constexpr (KIND == 2) {
-      // 2 (stability) = last tile warp (the lightest: padding tiles), 1 (cube-obstacle
-      // pairs) = the one before it; with a single tile warp it takes part 1
-      const int back = C.L.NW / 32 - (tid >> 5);
-      const int part = twin_ext == 2 ? 3 - back : back;
-      if (manip && back <= twin_ext) twin_tower_helper<R>(tw, C.rows, C.scr, lane, want_grad, pquad, part, twin_ext);
-    }
+    // ---- P2: leg, start terms, fixed obstacles
     // path length (trajopt.py:474-476): tile sum of the leg's squared components
     R dv = R(0);
     if (is_wp && t < T - 1 && j < J) dv = C.x[(wq + 1) * kXS + j] - qj;
@@ -1027,7 +1022,14 @@ __global__ void __launch_bounds__(MAXT, 1) k_solve_al(const TrajScene<R>* __rest
         const int bb = tid >> 5;
         const int w0 = bb * T;
         R qj = tlw.j < J ? C.x[w0 * kXS + tlw.j] : R(0);
-        tile_polish<R>(tlw, ch, qj, sc.pick_pos[bb], sc.pick_yaw[bb]);
+        int its = 0;
+        tile_polish<R>(tlw, ch, qj, sc.pick_pos[bb], sc.pick_yaw[bb], nullptr, 0, nullptr, 0, nullptr, &its);
+        if (C.prof.on && (tid & 31) == 0) {
+          atomicAdd(&g_al_polish[0], (unsigned long long)its);
+          atomicAdd(&g_al_polish[1], 1ull);
+          if (its >= kPolishMaxIters) atomicAdd(&g_al_polish[2], 1ull);
+          atomicMax(&g_al_polish[3], (unsigned long long)its);
+        }
         __syncwarp();  // the replica lanes' reads of x above precede lanes 0-7's writes
         if ((tid & 31) < kTile && tlw.j < J) C.x[w0 * kXS + tlw.j] = qj;
       }

@@ -262,8 +262,9 @@ __device__ __forceinline__ R tile_dls(const Tile& tl, const R (&col)[NR], const 
 // ik_solve_batch for one (target, restart) tile (robot.py:262-302). Lane j holds q_j;
 // returns ok and writes the score |pos err| + |yaw err| (uniform across the tile).
 template <typename R>
-__device__ bool tile_ik(const Tile& tl, const ChainDesc<R>& ch, R& qj, const R tp[3], R ty, int max_iters, R damping,
+__device__ bool tile_ik(const Tile& tl, const ChainDesc<R>& ch, R& q_io, const R tp[3], R ty, int max_iters, R damping,
                         R* score) {
+  R qj = q_io;
   const int j = tl.j;
   const bool live = j < ch.J;
   LaneChain<R> lc;
@@ -293,6 +294,7 @@ __device__ bool tile_ik(const Tile& tl, const ChainDesc<R>& ch, R& qj, const R t
   const R pn = Math<R>::sqrt_((pe[0] * pe[0] + pe[1] * pe[1]) + pe[2] * pe[2]);
   const R ye = fabs(wrap_yaw(ty - yaw_of(f.Ree)));
   *score = pn + ye;
+  q_io = qj;
   return pn < R(kIkPosTol) && ye < R(kIkYawTol);
 }
 
@@ -301,11 +303,12 @@ __device__ bool tile_ik(const Tile& tl, const ChainDesc<R>& ch, R& qj, const R t
 // tile's index once every restart has finished IK; a tile whose index `me` lost stops
 // polishing (its result is discarded, so the winner's result is unchanged).
 template <typename R>
-__device__ bool tile_polish(const Tile& tl, const ChainDesc<R>& ch, R& qj, const R tp[3], R ty,
+__device__ bool tile_polish(const Tile& tl, const ChainDesc<R>& ch, R& q_io, const R tp[3], R ty,
                             const volatile int* best = nullptr, int me = 0,
                             const volatile unsigned long long* cur = nullptr, unsigned long long mine = 0,
-                            bool* completed = nullptr) {
+                            bool* completed = nullptr, int* iters = nullptr) {
   if (completed) *completed = false;
+  R qj = q_io;  // iterate in a register (q_io may live in memory when this is not inlined)
   const int j = tl.j;
   const bool live = j < ch.J;
   const R cos_tol = R(0.99998750002604164);  // cos(0.005)
@@ -314,7 +317,8 @@ __device__ bool tile_polish(const Tile& tl, const ChainDesc<R>& ch, R& qj, const
   lc.load(ch, j);
   TileFrame<R> f;
   R prev1 = qj, prev2 = qj;
-  for (int it = 0; it < kPolishMaxIters; ++it) {
+  int it = 0;
+  for (; it < kPolishMaxIters; ++it) {
     if (best) {  // abort once another tile is the winner or the current best candidate
       int stop = 0;
       if (j == 0) {
@@ -322,7 +326,10 @@ __device__ bool tile_polish(const Tile& tl, const ChainDesc<R>& ch, R& qj, const
         stop = (b >= 0) ? (b != me) : (cur != nullptr && *cur != mine);
       }
       // any replica's lane 0 seeing the stop condition stops the whole tile / warp together
-      if (tl.any(stop != 0)) return false;
+      if (tl.any(stop != 0)) {
+        q_io = qj;
+        return false;
+      }
     }
     tile_fk(tl, lc, qj, f);
     const R pe[3] = {tp[0] - f.ee[0], tp[1] - f.ee[1], tp[2] - f.ee[2]};
@@ -344,10 +351,12 @@ __device__ bool tile_polish(const Tile& tl, const ChainDesc<R>& ch, R& qj, const
     }
     if (tile_settled(tl, qj, prev1, prev2, it, kPolishMaxIters)) break;
   }
+  if (iters) *iters = it;
   tile_fk(tl, lc, qj, f);
   const R pe[3] = {tp[0] - f.ee[0], tp[1] - f.ee[1], tp[2] - f.ee[2]};
   const R pn = Math<R>::sqrt_((pe[0] * pe[0] + pe[1] * pe[1]) + pe[2] * pe[2]);
   if (completed) *completed = true;
+  q_io = qj;
   return pn < R(kIkPosTol) && fabs(wrap_yaw(ty - yaw_of(f.Ree))) < R(kIkYawTol) && -f.Ree[8] > cos_tol;
 }
 

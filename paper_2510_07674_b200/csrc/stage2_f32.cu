@@ -24,3 +24,22 @@ extern "C" int spasm_al_profile(int enable, double* out) {
   }
   return SPASM_OK;
 }
+
+// Diagnostic: per-warp own-work cycles of the fp32 AL kernel's phases (AlProf::arrive, lane
+// 0 of every warp, summed over CTAs); out = 32 x 8 doubles [warp][phase] + 4 pick-polish
+// counters (iterations, calls, calls at the iteration cap, max iterations), then reset.
+extern "C" int spasm_al_profile_warps(double* out) {
+  using namespace spasm;
+  unsigned long long h[32][8];
+  SPASM_CUDA_TRY(cudaMemcpyFromSymbol(h, g_al_warp, sizeof(h)));
+  for (int w = 0; w < 32; ++w)
+    for (int k = 0; k < 8; ++k) out[w * 8 + k] = (double)h[w][k];
+  static const unsigned long long z[32][8] = {{0}};
+  SPASM_CUDA_TRY(cudaMemcpyToSymbol(g_al_warp, z, sizeof(z)));
+  unsigned long long pol[4];
+  SPASM_CUDA_TRY(cudaMemcpyFromSymbol(pol, g_al_polish, sizeof(pol)));
+  for (int k = 0; k < 4; ++k) out[256 + k] = (double)pol[k];
+  static const unsigned long long zp[4] = {0};
+  SPASM_CUDA_TRY(cudaMemcpyToSymbol(g_al_polish, zp, sizeof(zp)));
+  return SPASM_OK;
+}

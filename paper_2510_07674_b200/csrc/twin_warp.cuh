@@ -16,14 +16,8 @@
 
 namespace spasm {
 
-// scratch (elements of R) the warp twin needs for n bodies
-// (96 slot rows: the tower twin may hand parts to two helper warps, twin_tower_helper)
-__host__ __device__ inline int twin_warp_scratch(int n) { return 2 * n + 96 * 4 * n + 4; }
-
-// named barrier 1 between the aux warp (sync) and the tile warps that compute parts of the
-// tower twin (arrive); 32 threads per warp, every warp converged
-__device__ __forceinline__ void twin_ext_arrive(int count) { asm volatile("bar.arrive 1, %0;" ::"r"(count) : "memory"); }
-__device__ __forceinline__ void twin_ext_sync(int count) { asm volatile("bar.sync 1, %0;" ::"r"(count) : "memory"); }
+// scratch (elements of R) the warp twin needs for n bodies (32 lane slot rows)
+__host__ __device__ inline int twin_warp_scratch(int n) { return 2 * n + 32 * 4 * n + 4; }
 
 template <typename R>
 __device__ __forceinline__ R warp_sum_fixed(R v) {
@@ -171,11 +165,6 @@ __device__ __forceinline__ void twin_tower_obstacles(const TowerScene<R>& sc, co
   }
 }
 
-// Slot rows of the tower twin's work split: rows 0-31 the aux warp (pairs, heights and,
-// without helpers, everything), rows 32-63 the cube-obstacle pairs, rows 64-95 the
-// stability supports, each helper on a tile warp; helper costs follow the 96 rows.
-__host__ __device__ inline int twin_ext_count(int ext) { return 32 * (1 + ext); }
-
 // Items [it_lo, it_hi) of the tower twin (supports i < B-1, heights, cube pairs) and, when
 // `obstacles`, the cube-obstacle pairs, accumulated into this lane's slot row `my` (zeroed
 // here); returns the lane's cost.
@@ -261,44 +250,16 @@ __device__ R twin_tower_core(const TowerScene<R>& sc, const R* rows, R* my, int 
   return cost;
 }
 
-// One helper warp of the tower twin (part 1 = cube-obstacle pairs, 2 = stability supports):
-// fills its slot rows and cost, then arrives on named barrier 1 where the aux warp's
-// twin_tower_warp(ext) waits. The warp must be full and converged.
-template <typename R>
-__device__ void twin_tower_helper(const TowerScene<R>& sc, const R* rows, R* scr, int lane, bool want_grad, bool quad,
-                                  int part, int ext) {
-  const int n = sc.n_blocks, nv = 4 * n;
-  R* my = scr + 2 * n + (32 * part + lane) * nv;
-  const int lo = 0, hi = part == 2 ? n - 1 : 0;
-  const bool obs = part == 1;
-  R cost;
-  if (want_grad)
-    cost = quad ? twin_tower_core<R, true, true>(sc, rows, my, lane, lo, hi, obs)
-                : twin_tower_core<R, true, false>(sc, rows, my, lane, lo, hi, obs);
-  else
-    cost = quad ? twin_tower_core<R, false, true>(sc, rows, my, lane, lo, hi, obs)
-                : twin_tower_core<R, false, false>(sc, rows, my, lane, lo, hi, obs);
-  cost = warp_sum_fixed(cost);
-  if (lane == 0) scr[2 * n + 96 * nv + part - 1] = cost;
-  __syncwarp();
-  twin_ext_arrive(twin_ext_count(ext));
-}
-
-// ext = number of helper warps (0: the aux warp does all the work; 1: + cube-obstacle
-// pairs; 2: + stability supports)
+// The whole tower twin on the aux warp (the tile warps are the longer path through the
+// step: handing its parts to them lengthened the step).
 template <typename R, bool WG, bool Q>
-__device__ R twin_tower_warp(const TowerScene<R>& sc, const R* rows, R* grad, R* scr, int lane, int ext = 0) {
+__device__ R twin_tower_warp(const TowerScene<R>& sc, const R* rows, R* grad, R* scr, int lane) {
   const int n = sc.n_blocks;
   const int nv = 4 * n;
   R* gl = scr + 2 * n;
-  R cost = twin_tower_core<R, WG, Q>(sc, rows, gl + lane * nv, lane, ext >= 2 ? n - 1 : 0, 1 << 30, ext == 0);
+  R cost = twin_tower_core<R, WG, Q>(sc, rows, gl + lane * nv, lane, 0, 1 << 30, true);
   cost = warp_sum_fixed(cost);
-  if (ext) {
-    twin_ext_sync(twin_ext_count(ext));
-    cost += scr[2 * n + 96 * nv];
-    if (ext >= 2) cost += scr[2 * n + 96 * nv + 1];
-  }
-  twin_reduce_slots<R, WG>(gl, nv, grad, lane, 32 * (1 + ext));
+  twin_reduce_slots<R, WG>(gl, nv, grad, lane, 32);
   __syncwarp();
   return cost;
 }
@@ -306,8 +267,7 @@ __device__ R twin_tower_warp(const TowerScene<R>& sc, const R* rows, R* grad, R*
 // Cost of the placement twin on all 32 lanes of the calling warp; grad (4 per body)
 // written when want_grad.
 template <typename R, int KIND, int SPB, class TS>
-__device__ R twin_warp(const TS& ts, const R* rows, R* grad, R* scr, int lane, bool want_grad, bool quad,
-                      int ext = 0) {
+__device__ R twin_warp(const TS& ts, const R* rows, R* grad, R* scr, int lane, bool want_grad, bool quad) {
   if constexpr (KIND == 1) {
     if (want_grad)
       return quad ? twin_tetris_warp<R, SPB, true, true>(ts, rows, grad, scr, lane)
@@ -316,10 +276,10 @@ __device__ R twin_warp(const TS& ts, const R* rows, R* grad, R* scr, int lane, b
                 : twin_tetris_warp<R, SPB, false, false>(ts, rows, grad, scr, lane);
   } else if constexpr (KIND == 2) {
     if (want_grad)
-      return quad ? twin_tower_warp<R, true, true>(ts, rows, grad, scr, lane, ext)
-                  : twin_tower_warp<R, true, false>(ts, rows, grad, scr, lane, ext);
-    return quad ? twin_tower_warp<R, false, true>(ts, rows, grad, scr, lane, ext)
-                : twin_tower_warp<R, false, false>(ts, rows, grad, scr, lane, ext);
+      return quad ? twin_tower_warp<R, true, true>(ts, rows, grad, scr, lane)
+                  : twin_tower_warp<R, true, false>(ts, rows, grad, scr, lane);
+    return quad ? twin_tower_warp<R, false, true>(ts, rows, grad, scr, lane)
+                : twin_tower_warp<R, false, false>(ts, rows, grad, scr, lane);
   } else {
     return R(0);
   }

@@ -36,3 +36,15 @@ for k, n in names.items():
 print(f"  tile t0 sub-marks: leg+start done at {out[17] / max(1, outers):.0f}, B totals+pgsum done at "
       f"{out[19] / max(1, outers):.0f} cycles/outer (since the phase's start)")
 print(f"  aux P2 split: placed poses done at {out[25] / max(1, outers):.0f}, twin done at {out[26] / max(1, outers):.0f} cycles/outer")
+wp_all = np.zeros(32 * 8 + 4)
+lib.spasm_al_profile_warps(wp_all.ctypes.data)
+wp = wp_all[:256].reshape(32, 8) / max(1, outers)
+pol = wp_all[256:]
+print("per-warp own work (cycles/outer, summed over CTAs; since each phase's start):")
+print("  warp        P1        P2   (leg/start)       P3         B")
+for w in range(32):
+    if wp[w].sum() == 0:
+        continue
+    print(f"  {w:4d} {wp[w, 0]:9.0f} {wp[w, 1]:9.0f} {wp[w, 5]:9.0f} {wp[w, 2]:12.0f} {wp[w, 4]:9.0f}")
+print(f"pick polish: {pol[1]:.0f} calls, {pol[0] / max(1, pol[1]):.1f} iterations per call (max {pol[3]:.0f}), "
+      f"{pol[2]:.0f} at the {1000}-iteration cap")
