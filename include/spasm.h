@@ -367,6 +367,11 @@ int spasm_al_profile(int enable, double* out);
  * warp; out = 32 x 8 doubles [warp][phase], summed over CTAs) followed by 4 pick-polish
  * counters (iterations, calls, calls at the cap, max iterations); 260 doubles. Resets. */
 int spasm_al_profile_warps(double* out);
+/* Diagnostic: counters of the fp32 lift kernel k_ik_group, summed over CTAs (CTAs, cycles
+ * to the last restart's IK, cycles to the end, max / winner IK iterations, winner polish
+ * iterations after IK, speculatively completed polishes, all restarts' IK iterations).
+ * enable 1/0; out (8 doubles, optional) receives and resets them. */
+int spasm_ik_profile(int enable, double* out);
 
 #ifdef __cplusplus
 }

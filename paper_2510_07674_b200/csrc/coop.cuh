@@ -89,6 +89,20 @@ struct Tile {
   }
 };
 
+// normalize_yaw / np.mod with the fast-range test voted across the tile: the common case
+// takes the branch-free fold (same bits as wrap_yaw / np_mod_pos), the rare out-of-range
+// case the scalar routine, and the branch is tile-uniform (no reconvergence point).
+template <typename R>
+__device__ __forceinline__ R tile_wrap_yaw(const Tile& tl, R a) {
+  if (tl.all(wrap_yaw_in_fast_range(a))) return wrap_yaw_finish(wrap_yaw_fold(a + R(3.1415926535897932384626433832795)));
+  return wrap_yaw(a);
+}
+template <typename R>
+__device__ __forceinline__ R tile_np_mod_pos(const Tile& tl, R a, R m) {
+  if (tl.all(np_mod_in_fast_range(a, m))) return np_mod_finish(a >= m ? a - m : a, m);
+  return np_mod_pos(a, m);
+}
+
 // Per-lane frame of joint j after a tile FK:
 //   M   rotation before joint j (product of joints < j)     -> axis z = M * axis_j
 //   P   rotation after joint j (product of joints <= j)      -> link frame of link j
@@ -132,27 +146,25 @@ __device__ __forceinline__ void tile_fk(const Tile& tl, const LaneChain<R>& ch, 
   const int J = ch.J;
   const int j = tl.j;
   const bool live = j < J;
+  // Branch-free: every lane computes, lanes past the chain / below a scan level select
+  // (divergent branches here cost a reconvergence point each and split the scheduling
+  // blocks; the selected values are the same operations as before)
   R Rj[9];
-  if (live) {
-    rodrigues(ch.ax, qj, Rj);
-  } else {
+  rodrigues(ch.ax, qj, Rj);
 #pragma unroll
-    for (int k = 0; k < 9; ++k) Rj[k] = (k % 4 == 0) ? R(1) : R(0);
-  }
+  for (int k = 0; k < 9; ++k) Rj[k] = live ? Rj[k] : ((k % 4 == 0) ? R(1) : R(0));
   // inclusive prefix product P_j = R_0 R_1 ... R_j
 #pragma unroll
   for (int k = 0; k < 9; ++k) f.P[k] = Rj[k];
 #pragma unroll
   for (int d = 1; d < kTile; d <<= 1) {
-    R O[9];
+    R O[9], N[9];
 #pragma unroll
     for (int k = 0; k < 9; ++k) O[k] = tl.up(f.P[k], d);
-    if (j >= d) {
-      R N[9];
-      mat3_mul(O, f.P, N);
+    mat3_mul(O, f.P, N);
+    const bool up = j >= d;
 #pragma unroll
-      for (int k = 0; k < 9; ++k) f.P[k] = N[k];
-    }
+    for (int k = 0; k < 9; ++k) f.P[k] = up ? N[k] : f.P[k];
   }
   // exclusive product M_j (identity for joint 0)
   R M[9];
@@ -161,12 +173,13 @@ __device__ __forceinline__ void tile_fk(const Tile& tl, const LaneChain<R>& ch, 
     const R v = tl.up(f.P[k], 1);
     M[k] = j == 0 ? ((k % 4 == 0) ? R(1) : R(0)) : v;
   }
-  R t[3] = {R(0), R(0), R(0)};
-  if (live) {
-    mat3_vec(M, ch.off, t);
-    mat3_vec(M, ch.ax, f.z);
-  } else {
-    f.z[0] = f.z[1] = f.z[2] = R(0);
+  R t[3];
+  mat3_vec(M, ch.off, t);
+  mat3_vec(M, ch.ax, f.z);
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+    t[c] = live ? t[c] : R(0);
+    f.z[c] = live ? f.z[c] : R(0);
   }
   // inclusive prefix sum of the translations -> joint origins
 #pragma unroll
@@ -176,7 +189,7 @@ __device__ __forceinline__ void tile_fk(const Tile& tl, const LaneChain<R>& ch, 
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
       const R v = tl.up(f.o[c], d);
-      if (j >= d) f.o[c] = v + f.o[c];
+      f.o[c] = j >= d ? v + f.o[c] : f.o[c];
     }
   }
   // end effector from the last joint's frame (robot.py:136-141)
@@ -263,7 +276,7 @@ __device__ __forceinline__ R tile_dls(const Tile& tl, const R (&col)[NR], const 
 // returns ok and writes the score |pos err| + |yaw err| (uniform across the tile).
 template <typename R>
 __device__ bool tile_ik(const Tile& tl, const ChainDesc<R>& ch, R& q_io, const R tp[3], R ty, int max_iters, R damping,
-                        R* score) {
+                        R* score, int* iters = nullptr) {
   R qj = q_io;
   const int j = tl.j;
   const bool live = j < ch.J;
@@ -271,37 +284,97 @@ __device__ bool tile_ik(const Tile& tl, const ChainDesc<R>& ch, R& q_io, const R
   lc.load(ch, j);
   TileFrame<R> f;
   R prev1 = qj, prev2 = qj;
-  for (int it = 0; it < max_iters; ++it) {
+  int it = 0;
+  for (; it < max_iters; ++it) {
     tile_fk(tl, lc, qj, f);
     const R pe[3] = {tp[0] - f.ee[0], tp[1] - f.ee[1], tp[2] - f.ee[2]};
-    const R ye = wrap_yaw(ty - yaw_of(f.Ree));
+    const R ye = tile_wrap_yaw(tl, ty - yaw_of(f.Ree));
     const R pn = Math<R>::sqrt_((pe[0] * pe[0] + pe[1] * pe[1]) + pe[2] * pe[2]);
-    if (tl.all(pn < R(kIkPosTol) && fabs(ye) < R(kIkYawTol))) break;
+    const bool conv = pn < R(kIkPosTol) && fabs(ye) < R(kIkYawTol);
+    // the step is formed before the convergence vote (discarded on exit): the Jacobian and
+    // the DLS factorisation then overlap the yaw chain instead of waiting on the vote
     const R rel[3] = {f.ee[0] - f.o[0], f.ee[1] - f.o[1], f.ee[2] - f.o[2]};
     R c[3];
     cross3(f.z, rel, c);
     const R col[4] = {c[0], c[1], c[2], f.z[2]};
     const R e4[4] = {pe[0], pe[1], pe[2], ye};
     const R dq = tile_dls<R, 4>(tl, col, e4, damping);
-    if (live) {
-      const R v = qj + dq;
-      qj = v < lc.lo ? lc.lo : (v > lc.hi ? lc.hi : v);
-    }
+    if (tl.all(conv)) break;
+    const R v = qj + dq;
+    qj = live ? (v < lc.lo ? lc.lo : (v > lc.hi ? lc.hi : v)) : qj;
     if (tile_settled(tl, qj, prev1, prev2, it, max_iters)) break;
   }
+  if (iters) *iters = it;
   tile_fk(tl, lc, qj, f);
   const R pe[3] = {tp[0] - f.ee[0], tp[1] - f.ee[1], tp[2] - f.ee[2]};
   const R pn = Math<R>::sqrt_((pe[0] * pe[0] + pe[1] * pe[1]) + pe[2] * pe[2]);
-  const R ye = fabs(wrap_yaw(ty - yaw_of(f.Ree)));
+  const R ye = fabs(tile_wrap_yaw(tl, ty - yaw_of(f.Ree)));
   *score = pn + ye;
   q_io = qj;
   return pn < R(kIkPosTol) && ye < R(kIkYawTol);
 }
 
-// _polish_tool_down for one configuration on a tile (trajopt.py:726-776). Optional
-// speculative mode (k_ik_group): `best` points at a shared slot that becomes the winning
-// tile's index once every restart has finished IK; a tile whose index `me` lost stops
-// polishing (its result is discarded, so the winner's result is unchanged).
+// _polish_tool_down for one configuration on a tile (trajopt.py:726-776), as a resumable
+// iteration: begin() from a configuration, step() runs one loop iteration and returns true
+// once the loop has ended (converged, settled or at the cap), finish() is the final check.
+template <typename R>
+struct PolishRun {
+  LaneChain<R> lc;
+  R prev1, prev2;
+  int it;
+  bool live;
+  __device__ __forceinline__ void begin(const Tile& tl, const ChainDesc<R>& ch, R qj) {
+    lc.load(ch, tl.j);
+    live = tl.j < ch.J;
+    prev1 = prev2 = qj;
+    it = 0;
+  }
+  __device__ __forceinline__ bool step(const Tile& tl, R& qj, const R tp[3], R ty) {
+    if (it >= kPolishMaxIters) return true;
+    const R cos_tol = R(0.99998750002604164);  // cos(0.005)
+    const R two_pi = R(6.283185307179586476925286766559);
+    TileFrame<R> f;
+    tile_fk(tl, lc, qj, f);
+    const R pe[3] = {tp[0] - f.ee[0], tp[1] - f.ee[1], tp[2] - f.ee[2]};
+    const R ye = tile_wrap_yaw(tl, ty - yaw_of(f.Ree));
+    const R ax[3] = {f.Ree[2], f.Ree[5], f.Ree[8]};
+    const R pn = Math<R>::sqrt_((pe[0] * pe[0] + pe[1] * pe[1]) + pe[2] * pe[2]);
+    const bool conv = pn < R(kIkPosTol) && fabs(ye) < R(kIkYawTol) && -ax[2] > cos_tol;
+    // step formed before the convergence vote (discarded on exit), as in tile_ik
+    const R rel[3] = {f.ee[0] - f.o[0], f.ee[1] - f.o[1], f.ee[2] - f.o[2]};
+    R c[3], d[3];
+    cross3(f.z, rel, c);
+    cross3(f.z, ax, d);
+    const R yj = yaw_jac(f.Ree, f.z);
+    const R col[5] = {c[0], c[1], c[2], live ? yj : R(0), d[2]};
+    const R e5[5] = {pe[0], pe[1], pe[2], ye, R(-1) - ax[2]};
+    const R dq = tile_dls<R, 5>(tl, col, e5, R(kIkDamping));
+    if (tl.all(conv)) return true;
+    {  // branch-free update: every lane computes, lanes past the chain keep q
+      const R v0 = qj + dq;
+      const R vm = lc.lo + tile_np_mod_pos(tl, v0 - lc.lo, two_pi);
+      R v = lc.full ? vm : v0;
+      v = v < lc.lo ? lc.lo : (v > lc.hi ? lc.hi : v);
+      qj = live ? v : qj;
+    }
+    if (tile_settled(tl, qj, prev1, prev2, it, kPolishMaxIters)) return true;
+    ++it;
+    return it >= kPolishMaxIters;
+  }
+  __device__ __forceinline__ bool finish(const Tile& tl, R qj, const R tp[3], R ty) const {
+    const R cos_tol = R(0.99998750002604164);
+    TileFrame<R> f;
+    tile_fk(tl, lc, qj, f);
+    const R pe[3] = {tp[0] - f.ee[0], tp[1] - f.ee[1], tp[2] - f.ee[2]};
+    const R pn = Math<R>::sqrt_((pe[0] * pe[0] + pe[1] * pe[1]) + pe[2] * pe[2]);
+    return pn < R(kIkPosTol) && fabs(tile_wrap_yaw(tl, ty - yaw_of(f.Ree))) < R(kIkYawTol) && -f.Ree[8] > cos_tol;
+  }
+};
+
+// The whole polish of one configuration. Optional speculative mode (k_ik_group): `best`
+// points at a shared slot that becomes the winning tile's index once every restart has
+// finished IK; a tile whose index `me` lost stops polishing (its result is discarded, so
+// the winner's result is unchanged).
 template <typename R>
 __device__ bool tile_polish(const Tile& tl, const ChainDesc<R>& ch, R& q_io, const R tp[3], R ty,
                             const volatile int* best = nullptr, int me = 0,
@@ -309,19 +382,12 @@ __device__ bool tile_polish(const Tile& tl, const ChainDesc<R>& ch, R& q_io, con
                             bool* completed = nullptr, int* iters = nullptr) {
   if (completed) *completed = false;
   R qj = q_io;  // iterate in a register (q_io may live in memory when this is not inlined)
-  const int j = tl.j;
-  const bool live = j < ch.J;
-  const R cos_tol = R(0.99998750002604164);  // cos(0.005)
-  const R two_pi = R(6.283185307179586476925286766559);
-  LaneChain<R> lc;
-  lc.load(ch, j);
-  TileFrame<R> f;
-  R prev1 = qj, prev2 = qj;
-  int it = 0;
-  for (; it < kPolishMaxIters; ++it) {
+  PolishRun<R> run;
+  run.begin(tl, ch, qj);
+  for (;;) {
     if (best) {  // abort once another tile is the winner or the current best candidate
       int stop = 0;
-      if (j == 0) {
+      if (tl.j == 0) {
         const int b = *best;
         stop = (b >= 0) ? (b != me) : (cur != nullptr && *cur != mine);
       }
@@ -331,33 +397,12 @@ __device__ bool tile_polish(const Tile& tl, const ChainDesc<R>& ch, R& q_io, con
         return false;
       }
     }
-    tile_fk(tl, lc, qj, f);
-    const R pe[3] = {tp[0] - f.ee[0], tp[1] - f.ee[1], tp[2] - f.ee[2]};
-    const R ye = wrap_yaw(ty - yaw_of(f.Ree));
-    const R ax[3] = {f.Ree[2], f.Ree[5], f.Ree[8]};
-    const R pn = Math<R>::sqrt_((pe[0] * pe[0] + pe[1] * pe[1]) + pe[2] * pe[2]);
-    if (tl.all(pn < R(kIkPosTol) && fabs(ye) < R(kIkYawTol) && -ax[2] > cos_tol)) break;
-    const R rel[3] = {f.ee[0] - f.o[0], f.ee[1] - f.o[1], f.ee[2] - f.o[2]};
-    R c[3], d[3];
-    cross3(f.z, rel, c);
-    cross3(f.z, ax, d);
-    const R col[5] = {c[0], c[1], c[2], live ? yaw_jac(f.Ree, f.z) : R(0), d[2]};
-    const R e5[5] = {pe[0], pe[1], pe[2], ye, R(-1) - ax[2]};
-    const R dq = tile_dls<R, 5>(tl, col, e5, R(kIkDamping));
-    if (live) {
-      R v = qj + dq;
-      if (lc.full) v = lc.lo + np_mod_pos(v - lc.lo, two_pi);
-      qj = v < lc.lo ? lc.lo : (v > lc.hi ? lc.hi : v);
-    }
-    if (tile_settled(tl, qj, prev1, prev2, it, kPolishMaxIters)) break;
+    if (run.step(tl, qj, tp, ty)) break;
   }
-  if (iters) *iters = it;
-  tile_fk(tl, lc, qj, f);
-  const R pe[3] = {tp[0] - f.ee[0], tp[1] - f.ee[1], tp[2] - f.ee[2]};
-  const R pn = Math<R>::sqrt_((pe[0] * pe[0] + pe[1] * pe[1]) + pe[2] * pe[2]);
+  if (iters) *iters = run.it;
   if (completed) *completed = true;
   q_io = qj;
-  return pn < R(kIkPosTol) && fabs(wrap_yaw(ty - yaw_of(f.Ree))) < R(kIkYawTol) && -f.Ree[8] > cos_tol;
+  return run.finish(tl, qj, tp, ty);
 }
 
 // largest arm-sphere penetration (no clamp) against a sphere set (trajopt.py:779-787)

@@ -151,36 +151,55 @@ __device__ __forceinline__ R yaw_of(const R* Rm) {
   return Math<R>::atan2_(Rm[3], Rm[0]);
 }
 
+// normalize_yaw pieces: x = a + pi in (-2m, 2m) (m = 2 pi; every yaw difference here) is
+// the fast range, where fmod(x, m) is x, x - m or x + m, each exact (Sterbenz), so the fold
+// gives fmod's bits without its loop (fmod(-m, m) = -0 vs +0 here: both fail the w < 0
+// test of the finish, same result)
+template <typename R>
+__device__ __forceinline__ bool wrap_yaw_in_fast_range(R a) {
+  const R two_pi = R(6.283185307179586476925286766559);
+  const R x = a + R(3.1415926535897932384626433832795);
+  return x > -R(2) * two_pi && x < R(2) * two_pi;
+}
+template <typename R>
+__device__ __forceinline__ R wrap_yaw_fold(R x) {
+  const R two_pi = R(6.283185307179586476925286766559);
+  return x >= two_pi ? x - two_pi : (x <= -two_pi ? x + two_pi : x);
+}
+template <typename R>
+__device__ __forceinline__ R wrap_yaw_finish(R w) {
+  const R two_pi = R(6.283185307179586476925286766559);
+  const R pi = R(3.1415926535897932384626433832795);
+  w = w < R(0) ? w + two_pi : w;
+  w -= pi;
+  return w <= -pi ? w + two_pi : w;
+}
+
 // normalize_yaw: wrap into (-pi, pi] (geometry.py:31-38; numpy remainder semantics)
 template <typename R>
 __device__ __forceinline__ R wrap_yaw(R a) {
   const R two_pi = R(6.283185307179586476925286766559);
   const R pi = R(3.1415926535897932384626433832795);
-  // x in (-2m, 2m) (every yaw difference here): fmod is x, x - m or x + m, each exact
-  // (Sterbenz), so the branch gives fmod's bits without its loop (fmod(-m, m) = -0 vs
-  // +0 here: both fail the w < 0 test below, same result)
   const R x = a + pi;
-  R w = (x > -R(2) * two_pi && x < R(2) * two_pi)
-            ? (x >= two_pi ? x - two_pi : (x <= -two_pi ? x + two_pi : x))
-            : fmod(x, two_pi);
-  if (w < R(0)) w += two_pi;
-  w -= pi;
-  if (w <= -pi) w += two_pi;
-  return w;
+  R w = wrap_yaw_in_fast_range(a) ? wrap_yaw_fold(x) : fmod(x, two_pi);
+  return wrap_yaw_finish(w);
 }
 
 // np.mod(a, m) for m > 0 (npy_divmod: result carries the divisor's sign)
+// a in [-m, 2m) (a clamped joint plus a step <= 0.5 rad) is the fast range: fmod is a - m
+// or a, and a - m is exact there (Sterbenz), so the fold gives fmod's bits without its loop
+template <typename R>
+__device__ __forceinline__ bool np_mod_in_fast_range(R a, R m) {
+  return a >= -m && a < R(2) * m;
+}
+template <typename R>
+__device__ __forceinline__ R np_mod_finish(R r, R m) {
+  return r != R(0) ? (r < R(0) ? r + m : r) : R(0);
+}
 template <typename R>
 __device__ __forceinline__ R np_mod_pos(R a, R m) {
-  // a in [-m, 2m) (a clamped joint plus a step <= 0.5 rad): fmod is a - m or a, and a - m
-  // is exact there (Sterbenz), so the branch below gives fmod's bits without its loop
-  R r = (a >= -m && a < R(2) * m) ? (a >= m ? a - m : a) : fmod(a, m);
-  if (r != R(0)) {
-    if (r < R(0)) r += m;
-  } else {
-    r = R(0);
-  }
-  return r;
+  const R r = np_mod_in_fast_range(a, m) ? (a >= m ? a - m : a) : fmod(a, m);
+  return np_mod_finish(r, m);
 }
 
 // d yaw / d q_j from dR/dq_j = [z_j]x R; 0 near gimbal (den < 1e-12)
@@ -188,11 +207,11 @@ template <typename R>
 __device__ __forceinline__ R yaw_jac(const R* Rm, const R* z) {
   const R r00 = Rm[0], r10 = Rm[3], r20 = Rm[6];
   const R den = r00 * r00 + r10 * r10;
-  if (den < R(1e-12)) return R(0);
   // dcol0 = z x col0
   const R dx = z[1] * r20 - z[2] * r10;
   const R dy = z[2] * r00 - z[0] * r20;
-  return (r00 * dy - r10 * dx) / den;
+  const R v = (r00 * dy - r10 * dx) / den;
+  return den < R(1e-12) ? R(0) : v;  // a select: no branch in the DLS loops
 }
 
 template <typename R>

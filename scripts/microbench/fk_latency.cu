@@ -68,6 +68,20 @@ __global__ void k_lds(const float* g, int iters, float* out, long long* cyc) {
   out[threadIdx.x] = k;
 }
 
+__global__ void k_atan2_cmp(unsigned long long n, unsigned long long seed, unsigned long long* bad) {
+  unsigned long long i = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x;
+  unsigned long long nb = 0;
+  for (; i < n; i += (unsigned long long)gridDim.x * blockDim.x) {
+    unsigned long long h = (i + seed) * 0x9E3779B97F4A7C15ull;
+    h ^= h >> 31; h *= 0xBF58476D1CE4E5B9ull; h ^= h >> 29;
+    float y = __uint_as_float((unsigned)h), x = __uint_as_float((unsigned)(h >> 32));
+    if (i & 1) { y = (float)((int)(h & 0xffff) - 32768) * 1e-4f; x = (float)((int)((h >> 16) & 0xffff) - 32768) * 1e-4f; }
+    const float a = atan2f(y, x), b = atan2_nobranch(y, x);
+    if (__float_as_uint(a) != __float_as_uint(b) && !(a != a && b != b)) ++nb;
+  }
+  atomicAdd(bad, nb);
+}
+
 int main2();
 int main() {
   ChainDesc<float> h{};
@@ -91,6 +105,12 @@ int main() {
     printf("shfl+fadd    %3d threads: %lld cycles/iter\n", threads, hc[0]);
     k_lds<<<1, threads>>>(nullptr, 1000, out, cyc); cudaMemcpy(hc, cyc, 8, cudaMemcpyDeviceToHost);
     printf("lds chain    %3d threads: %lld cycles/iter\n", threads, hc[0]);
+  }
+  {
+    unsigned long long* bad; cudaMalloc(&bad, 8); cudaMemset(bad, 0, 8);
+    k_atan2_cmp<<<1184, 256>>>(1ull << 28, 12345, bad);
+    unsigned long long hb; cudaMemcpy(&hb, bad, 8, cudaMemcpyDeviceToHost);
+    printf("atan2_nobranch vs atan2f: %llu mismatches in 2^28 inputs\n", hb);
   }
   return main2();
 }
@@ -141,10 +161,46 @@ __global__ void k_redux_lat(int iters, float* out, long long* cyc) {
   out[threadIdx.x] = (float)v;
 }
 
+__global__ void k_polstep(const ChainDesc<float>* g_ch, int iters, float* out, long long* cyc) {
+  __shared__ ChainDesc<float> ch;
+  if (threadIdx.x == 0) ch = *g_ch;
+  __syncthreads();
+  const Tile tl = Tile::make_warp();
+  PolishRun<float> run;
+  float q = 0.3f + 0.05f * tl.j;
+  const float tp[3] = {0.9f, 0.3f, 0.2f};
+  run.begin(tl, ch, q);
+  long long t0 = clock64();
+  int n = 0;
+  for (int i = 0; i < iters; ++i) {
+    run.it = 0;  // keep iterating (no cap)
+    run.step(tl, q, tp, 0.4f);
+    ++n;
+  }
+  long long t1 = clock64();
+  if (threadIdx.x == 0) cyc[blockIdx.x] = (t1 - t0) / n;
+  out[threadIdx.x] = q;
+}
+
 int main2() {
   float* out; cudaMalloc(&out, 4096 * 4);
   long long* cyc; cudaMalloc(&cyc, 64 * 8);
   long long hc[1];
+  {
+    ChainDesc<float> h{};
+    h.J = 7;
+    for (int j = 0; j < 7; ++j) {
+      h.axis[j][1] = (j % 2 == 1); h.axis[j][2] = (j % 2 == 0);
+      h.offset[j][2] = 0.2f;
+      h.lo[j] = -3.f; h.hi[j] = 3.f; h.full_circle[j] = 0;
+    }
+    for (int c = 0; c < 9; ++c) h.tool_R[c] = (c % 4 == 0);
+    ChainDesc<float>* d; cudaMalloc(&d, sizeof(h)); cudaMemcpy(d, &h, sizeof(h), cudaMemcpyHostToDevice);
+    for (int threads : {32, 128, 704}) {
+      k_polstep<<<1, threads>>>(d, 500, out, cyc); cudaMemcpy(hc, cyc, 8, cudaMemcpyDeviceToHost);
+      printf("polish step (FK + DLS<5> + checks) %3d threads: %lld cycles/iter\n", threads, hc[0]);
+    }
+  }
   k_dls_redux<<<1, 32>>>(1000, out, cyc); cudaMemcpy(hc, cyc, 8, cudaMemcpyDeviceToHost);
   printf("tile_dls<5> with REDUX max, 32 threads: %lld cycles/call\n", hc[0]);
   k_redux_lat<<<1, 32>>>(1000, out, cyc); cudaMemcpy(hc, cyc, 8, cudaMemcpyDeviceToHost);
