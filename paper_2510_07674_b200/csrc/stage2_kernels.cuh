@@ -216,174 +216,6 @@ __global__ void __launch_bounds__(MAXT) k_ik_group(const TrajScene<R>* __restric
   }
 }
 
-// Lift variant with a dedicated polisher warp (polish on, <= 16 restarts, one CTA per SM).
-// Warp 0 (SMSP 0 to itself) polishes; restart r runs its IK on warp r + r/3 + 1, i.e. on
-// the warps of SMSPs 1-3 (warps 4, 8, ... exit at once). A restart publishes its IK result
-// and key in shared memory and exits; the polisher polishes the best published candidate
-// (speculation by the fp32 image of the key, restart index on ties), switches when a better
-// one appears, and once the last restart has fixed the exact first-minimum winner (s_best)
-// finishes the winner's polish -- already done when the speculation held -- and writes the
-// group's outputs. Same results as k_ik_group: the polish is a pure function of the winner's
-// IK solution. Against k_ik_group the winner's serial polish no longer shares an SMSP with
-// three restarts' IK iterations (the lift's critical path, ik_profile: 2-3x slower there).
-constexpr int kIkPolWarps = 22;  // 16 restarts + polisher + idle warps 4, 8, 12, 16, 20
-
-__host__ __device__ inline int ik_pol_warps(int restarts) {
-  const int r = restarts - 1;
-  return r + r / 3 + 2;
-}
-
-template <typename R>
-__global__ void __launch_bounds__(kIkPolWarps * 32) k_ik_group_pol(
-    const TrajScene<R>* __restrict__ g_scene, int n_targets, int n_draws, uint64_t seed, uint64_t draw_stride,
-    int restarts, int max_iters, double damping, const double* __restrict__ tpos_in,
-    const double* __restrict__ tyaw_in, const double* __restrict__ rows, int D, int score_statics, IkOut out,
-    const int32_t* __restrict__ n_rows) {
-  if (n_rows && (int)(blockIdx.x % n_targets) >= g_scene->B + *n_rows * g_scene->B) return;
-  __shared__ ChainDesc<R> ch_s;
-  __shared__ R s_key[16], s_score[16], s_q[16][kMaxJ];
-  __shared__ int s_ok[16], s_pub[16], s_its[16];
-  __shared__ int s_best, s_done, s_gen;
-  const bool prof = g_ik_prof_on != 0;
-  const long long t_start = prof ? clock64() : 0;
-  if (threadIdx.x < 16) s_pub[threadIdx.x] = 0;
-  if (threadIdx.x == 0) {
-    s_best = -1;
-    s_done = 0;
-    s_gen = 0;
-  }
-  const TrajScene<R>& sc = *g_scene;
-  {
-    const int4* src = reinterpret_cast<const int4*>(&sc.ch);
-    int4* dst = reinterpret_cast<int4*>(&ch_s);
-    for (int i = threadIdx.x; i < (int)(sizeof(ChainDesc<R>) / sizeof(int4)); i += blockDim.x) dst[i] = src[i];
-  }
-  __syncthreads();  // the only CTA barrier: warps leave independently from here on
-  const ChainDesc<R>& ch = ch_s;
-  const int grp = blockIdx.x;
-  const int a = grp / n_targets, t = grp - a * n_targets;
-  const int J = ch.J;
-  const Tile tl = Tile::make_warp();  // 4 identical replicas per warp: warp-wide shuffles
-  const int warp = threadIdx.x >> 5;
-  const bool lane0 = (threadIdx.x & 31) == 0;
-  const int r = warp - 1 - warp / 4;  // restart of an IK warp
-  const bool ik_warp = warp >= 1 && (warp & 3) != 0 && r < restarts;
-  if (!ik_warp && warp != 0) return;
-  R tp[3], ty;
-  if (tpos_in) {
-    tp[0] = (R)tpos_in[3 * t];
-    tp[1] = (R)tpos_in[3 * t + 1];
-    tp[2] = (R)tpos_in[3 * t + 2];
-    ty = (R)tyaw_in[t];
-  } else {
-    lift_target<R>(sc, rows, D, t, tp, &ty);
-  }
-  if (__all_sync(0xffffffffu, ik_warp)) {
-    R qj = R(0);
-    if (tl.j < J) {
-      // seeds[t] = uniform(lower, upper, (restarts, dof)) of SeedSequence(seed, (t,)) (robot.py:255-257)
-      Pcg64 g;
-      g.init(seedseq_pcg64_dev(seed + (uint64_t)a * draw_stride, (uint64_t)t));
-      g.advance((uint64_t)r * J + tl.j);
-      const double lo = ch.lo64[tl.j], hi = ch.hi64[tl.j];
-      qj = (R)__dadd_rn(lo, __dmul_rn(__dsub_rn(hi, lo), g.next_double()));  // no FMA: numpy's rounding
-    }
-    R score;
-    int its = 0;
-    const bool ok = tile_ik<R>(tl, ch, qj, tp, ty, max_iters, R(damping), &score, &its);
-    if ((threadIdx.x & 31) < kTile && tl.j < J) s_q[r][tl.j] = qj;
-    __threadfence_block();
-    __syncwarp();
-    if (lane0) {
-      s_key[r] = (ok ? R(0) : R(1e6)) + score;
-      s_score[r] = score;
-      s_ok[r] = ok;
-      s_its[r] = its;
-      __threadfence_block();
-      *((volatile int*)&s_pub[r]) = 1;
-      atomicAdd(&s_gen, 1);
-      if (atomicAdd(&s_done, 1) == restarts - 1) {  // the last restart picks the first minimum (np.argmin)
-        __threadfence_block();
-        int b = 0;
-        for (int q = 1; q < restarts; ++q)
-          if (((volatile R*)s_key)[q] < ((volatile R*)s_key)[b]) b = q;
-        *((volatile int*)&s_best) = b;
-        if (prof) {
-          atomicAdd(&g_ik_prof[1], (unsigned long long)(clock64() - t_start));
-          int mx = 0;
-          unsigned long long sum = 0;
-          for (int q = 0; q < restarts; ++q) {
-            mx = max(mx, ((volatile int*)s_its)[q]);
-            sum += ((volatile int*)s_its)[q];
-          }
-          atomicAdd(&g_ik_prof[3], (unsigned long long)mx);
-          atomicAdd(&g_ik_prof[4], (unsigned long long)((volatile int*)s_its)[b]);
-          atomicAdd(&g_ik_prof[7], sum);
-        }
-      }
-    }
-    return;
-  }
-  // ---- warp 0: the polisher
-  const int lane = threadIdx.x & 31;
-  PolishRun<R> run;
-  R qj = R(0);
-  int cur = -1, gen_seen = -1, spec = -1;
-  bool fin = false, hit = false;
-  for (;;) {
-    const int b = __shfl_sync(0xffffffffu, *((volatile int*)&s_best), 0);
-    int target = b;
-    if (b < 0) {
-      const int gen = __shfl_sync(0xffffffffu, *((volatile int*)&s_gen), 0);
-      if (gen != gen_seen) {  // new publications: the best (fp32 key image, restart) so far
-        gen_seen = gen;
-        unsigned k = 0xffffffffu;
-        if (lane < restarts && *((volatile int*)&s_pub[lane])) {
-          __threadfence_block();
-          k = (order_key((float)((volatile R*)s_key)[lane]) & ~31u) | (unsigned)lane;
-        }
-        const unsigned m = __reduce_min_sync(0xffffffffu, k);
-        spec = m == 0xffffffffu ? -1 : (int)(m & 31u);
-      }
-      target = spec;
-    } else if (cur == b && !hit) {
-      hit = true;  // the speculation held when the winner became known
-    }
-    if (target < 0) {
-      __nanosleep(64);
-      continue;
-    }
-    if (target != cur) {
-      __threadfence_block();
-      cur = target;
-      qj = tl.j < J ? ((volatile R*)s_q[cur])[tl.j] : R(0);
-      run.begin(tl, ch, qj);
-      fin = false;
-    }
-    if (!fin) fin = run.step(tl, qj, tp, ty);
-    else if (b >= 0) break;
-    else __nanosleep(64);
-  }
-  const int b = cur;
-  const bool pol = run.finish(tl, qj, tp, ty);
-  R pen = R(0);
-  if (score_statics && sc.n_static > 0) pen = tile_arm_worst_pen<R>(tl, ch, qj, sc.st_c, sc.st_r, sc.n_static);
-  if (prof && lane0) {
-    atomicAdd(&g_ik_prof[0], 1ull);
-    atomicAdd(&g_ik_prof[2], (unsigned long long)(clock64() - t_start));
-    atomicAdd(&g_ik_prof[5], (unsigned long long)run.it);
-    if (hit) atomicAdd(&g_ik_prof[6], 1ull);
-  }
-  if (lane >= kTile) return;
-  if (tl.j < J) reinterpret_cast<R*>(out.sol)[(int64_t)grp * J + tl.j] = qj;
-  if (tl.j == 0) {
-    out.ik_ok[grp] = (uint8_t)s_ok[b];
-    if (out.pol_ok) out.pol_ok[grp] = (uint8_t)pol;
-    reinterpret_cast<R*>(out.score)[grp] = s_score[b];
-    if (out.pen) reinterpret_cast<R*>(out.pen)[grp] = pen;
-  }
-}
-
 // polish a batch of configurations (the _polish_tool_down API), one tile per row
 template <typename R>
 __global__ void k_polish(const TrajScene<R>* __restrict__ g_scene, int n, R* __restrict__ Q,

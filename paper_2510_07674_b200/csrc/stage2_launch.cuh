@@ -164,11 +164,7 @@ int launch_ik(const Traj& tr, int n_targets, int n_draws, uint64_t seed, uint64_
   const int64_t groups = (int64_t)n_targets * n_draws;
   const int bs = restarts * 32;  // one warp per restart tile (k_ik_group)
   const int64_t grid = groups;
-  if (polish && restarts <= 16 && grid <= kNumSMs) {  // dedicated polisher warp, one CTA per SM
-    k_ik_group_pol<R><<<(unsigned)grid, ik_pol_warps(restarts) * 32, 0, s>>>(
-        tr.dev<R>(), n_targets, n_draws, seed, stride, restarts, max_iters, damping, tpos, tyaw, rows, D,
-        score_statics, out, n_rows);
-  } else if (bs <= 512 && grid <= kNumSMs)
+  if (bs <= 512 && grid <= kNumSMs)
     k_ik_group<R, 512><<<(unsigned)grid, bs, 0, s>>>(tr.dev<R>(), n_targets, n_draws, seed, stride, restarts,
                                                      max_iters, damping, tpos, tyaw, rows, D, polish, score_statics, out,
                                                      n_rows);
