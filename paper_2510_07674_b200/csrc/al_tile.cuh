@@ -154,6 +154,27 @@ struct AlCtx {
   TrajScene<R>* sc;
   R *x, *g, *unit, *ee, *rot, *armw, *ga, *hp, *gh, *pg, *pl, *psi, *cp, *sp, *rows, *gpose, *scr, *pgsum, *red, *scal;
   int* flags;
+  // this thread's waypoint geometry, fixed for the launch: formed once (geom) instead of
+  // re-derived (an integer division, dependent shared-memory loads) at every inner step
+  int g_b, g_t, g_h0, g_nh, g_f0, g_f1, g_slo, g_shi;
+  bool g_manip, g_interior;
+
+  // after the scene is resident in shared memory (al_load)
+  __device__ void geom(int T) {
+    const int tid = threadIdx.x;
+    const int w = tid >> 3, j = tid & 7;
+    const bool is_wp = tid < L.NW && w < L.W;
+    g_manip = sc->manip != 0;
+    g_b = is_wp ? w / T : 0;
+    g_t = is_wp ? w - g_b * T : 0;
+    g_interior = g_manip && g_t >= 1 && g_t <= T - 2;
+    g_h0 = g_manip ? sc->blk_start[g_b] : 0;
+    g_nh = g_manip ? sc->blk_start[g_b + 1] - g_h0 : 0;
+    g_f0 = g_manip ? sc->blk_start[g_b + 1] : 0;
+    g_f1 = g_manip ? sc->n_blk : 0;
+    g_slo = j < L.J ? sc->ch.link_start[j] : 0;
+    g_shi = j < L.J ? sc->ch.link_start[j + 1] : 0;
+  }
 
   __device__ void bind(unsigned char* base, const AlLayout& l) {
     L = l;
@@ -317,7 +338,7 @@ __device__ __forceinline__ void al_eval(AlCtx<R>& C, const typename TwinSceneOf<
   const int tid = threadIdx.x;
   // sizes from the kernel-parameter layout (uniform to the compiler; equal to the scene's)
   const int W = C.L.W, J = C.L.J, T = prm.T, B = C.L.B, S = C.L.S, SBn = C.L.SB;
-  const bool manip = sc.manip != 0;
+  const bool manip = C.g_manip;
   const bool is_aux = tid >= C.L.NW;
   const int lane = tid & 31;
   const int w = tid >> 3;
@@ -325,12 +346,9 @@ __device__ __forceinline__ void al_eval(AlCtx<R>& C, const typename TwinSceneOf<
   const Tile tl = Tile::make();
   const Tile tlw = Tile::make_warp();  // for the calls every lane of the warp reaches
   const int j = tl.j;
-  const int b = is_wp ? w / T : 0;
-  const int t = is_wp ? w - b * T : 0;
-  const bool interior = manip && t >= 1 && t <= T - 2;
-  const int h0 = manip ? sc.blk_start[b] : 0;
-  const int nh = manip ? sc.blk_start[b + 1] - h0 : 0;
-  const int f0 = manip ? sc.blk_start[b + 1] : 0, f1 = manip ? sc.n_blk : 0;
+  const int b = C.g_b, t = C.g_t;
+  const bool interior = C.g_interior;
+  const int h0 = C.g_h0, nh = C.g_nh, f0 = C.g_f0, f1 = C.g_f1;
   const R w_start = R(prm.w_start);
   const int bar_count = C.L.NW + 32;
   WpState<R> st;
@@ -415,7 +433,7 @@ __device__ __forceinline__ void al_eval(AlCtx<R>& C, const typename TwinSceneOf<
           for (int c = 0; c < 9; ++c) C.rot[w * 9 + c] = f.Ree[c];
         }
         if (j < J)
-          for (int s = ch.link_start[j]; s < ch.link_start[j + 1]; ++s) tile_sphere(ch, f, s, C.armw + (w * S + s) * 3);
+          for (int s = C.g_slo; s < C.g_shi; ++s) tile_sphere(ch, f, s, C.armw + (w * S + s) * 3);
         if (interior) {  // held block = Ree @ FLIP @ u + ee (trajopt.py:441-447)
           for (int s = j; s < nh; s += kTile) {
             const R ux = sc.bu[h0 + s][0], uy = sc.bu[h0 + s][1], uz = sc.bu[h0 + s][2];
@@ -565,7 +583,7 @@ __device__ __forceinline__ void al_eval(AlCtx<R>& C, const typename TwinSceneOf<
       // arm: suffix sums over links >= k of (g, a x g), lane k = joint k (trajopt.py:586-590)
       R G[3] = {R(0), R(0), R(0)}, Mv[3] = {R(0), R(0), R(0)};
       if (is_wp && j < J) {
-        for (int s = ch.link_start[j]; s < ch.link_start[j + 1]; ++s) {
+        for (int s = C.g_slo; s < C.g_shi; ++s) {
           const R* a = C.armw + (w * S + s) * 3;
           const R* gg = C.ga + (w * S + s) * 3;
           R m[3];
@@ -902,6 +920,7 @@ __global__ void __launch_bounds__(kMaxAlThreads) k_al_eval(const TrajScene<R>* _
   const int64_t p = blockIdx.x;
   al_load(C, g_scene, values, p);
   const auto& tws = twin_smem(smem, L, tw);
+  C.geom(prm.T);
   if (threadIdx.x == 0) {
     C.scal[kLam0] = lam ? lam[3 * p] : R(0);
     C.scal[kLam1] = lam ? lam[3 * p + 1] : R(0);
@@ -942,6 +961,7 @@ __global__ void __launch_bounds__(kMaxAlThreads) k_validate(const TrajScene<R>* 
   const int64_t p = blockIdx.x;
   al_load(C, g_scene, values, p);
   const auto& tws = twin_smem(smem, L, tw);
+  C.geom(prm.T);
   al_eval<R, KIND, SPB>(C, tws, prm, false, false, false, R(0));  // FK tables for the current x
   al_validate<R, KIND, SPB>(C, tws, prm);
   if (threadIdx.x == 0) {
@@ -985,6 +1005,7 @@ __global__ void __launch_bounds__(MAXT, 1) k_solve_al(const TrajScene<R>* __rest
   if (rec.n_active && p >= *rec.n_active) return;
   al_load(C, g_scene, values, p);
   const auto& tws = twin_smem(smem, L, tw);
+  C.geom(prm.T);
   const TrajScene<R>& sc = *C.sc;
   const ChainDesc<R>& ch = sc.ch;
   const int tid = threadIdx.x;
