@@ -47,8 +47,8 @@ constexpr int kXS = 8;  // row stride of x / g / unit in shared memory ([w][join
 constexpr int kAlItems = 3;  // sphere items per tile lane (arm + held spheres of a waypoint <= 24)
 
 struct AlLayout {
-  int W, NW, nthreads, nwarps, J, B, T, S, SB, NB;
-  int scene, twin, x, g, unit, ee, rot, armw, ga, hp, gh, pg, pl, seg, rows, gpose, scr, pgsum, red, scal, flags;
+  int W, NW, NA, nthreads, nwarps, J, B, T, S, SB, NB;  // NA: aux warps (2 when B > 4 fits)
+  int scene, twin, x, g, unit, ee, rot, armw, ga, hp, gh, pg, pl, pyaw, seg, rows, gpose, scr, pgsum, red, scal, flags;
   int total;
 };
 
@@ -57,7 +57,10 @@ __host__ __device__ inline AlLayout al_layout(int B, int T, int J, int S, int SB
   AlLayout L;
   L.W = B * T;
   L.NW = (L.W * kTile + 31) / 32 * 32;
-  L.nthreads = L.NW + 32;
+  // B > 4 placed poses take two rounds of the aux warp's 4 FK tiles; a second aux warp runs
+  // blocks 4-7 in parallel when the block size allows
+  L.NA = (B > 4 && L.NW + 64 <= kMaxAlThreads) ? 2 : 1;
+  L.nthreads = L.NW + 32 * L.NA;
   L.nwarps = L.nthreads / 32;
   L.J = J;
   L.B = B;
@@ -88,6 +91,7 @@ __host__ __device__ inline AlLayout al_layout(int B, int T, int J, int S, int SB
   L.gh = take(3 * (SB > 0 ? SB : 1) * W * r);
   L.pg = take(8 * B * W * r);
   L.pl = take(3 * (NB > 0 ? NB : 1) * r);
+  L.pyaw = take(2 * (NB > 0 ? NB : 1) * r);  // d(placed sphere xy)/d(block yaw)
   L.seg = take(3 * B * r);  // psi | cp | sp
   L.rows = take(4 * B * r);
   L.gpose = take(4 * B * r);
@@ -145,6 +149,10 @@ __device__ __forceinline__ void bar_placed_arrive(int count) {
   asm volatile("bar.arrive 2, %0;" ::"r"(count) : "memory");
 }
 __device__ __forceinline__ void bar_placed_sync(int count) { asm volatile("bar.sync 2, %0;" ::"r"(count) : "memory"); }
+// named barrier 1 between the two aux warps (NA = 2): the second arrives after its placed
+// poses, the first syncs before the placement twin reads all of them
+__device__ __forceinline__ void bar_aux_arrive() { asm volatile("bar.arrive 1, 64;" ::: "memory"); }
+__device__ __forceinline__ void bar_aux_sync() { asm volatile("bar.sync 1, 64;" ::: "memory"); }
 
 
 template <typename R>
@@ -152,7 +160,7 @@ struct AlCtx {
   AlProf prof;
   AlLayout L;
   TrajScene<R>* sc;
-  R *x, *g, *unit, *ee, *rot, *armw, *ga, *hp, *gh, *pg, *pl, *psi, *cp, *sp, *rows, *gpose, *scr, *pgsum, *red, *scal;
+  R *x, *g, *unit, *ee, *rot, *armw, *ga, *hp, *gh, *pg, *pl, *pyaw, *psi, *cp, *sp, *rows, *gpose, *scr, *pgsum, *red, *scal;
   int* flags;
   // this thread's waypoint geometry, fixed for the launch: formed once (geom) instead of
   // re-derived (an integer division, dependent shared-memory loads) at every inner step
@@ -190,6 +198,7 @@ struct AlCtx {
     gh = reinterpret_cast<R*>(base + L.gh);
     pg = reinterpret_cast<R*>(base + L.pg);
     pl = reinterpret_cast<R*>(base + L.pl);
+    pyaw = reinterpret_cast<R*>(base + L.pyaw);
     psi = reinterpret_cast<R*>(base + L.seg);
     cp = psi + L.B;
     sp = cp + L.B;
@@ -317,6 +326,27 @@ __device__ __forceinline__ R pens_fixed_all(const TrajScene<R>& sc, const R* c, 
   return v;
 }
 
+// One sphere (c, radius rr) against the placed spheres [q0, q1) of one block: adds the
+// penetration sum to v, the position slope sum to (ax, ay, az) and the yaw slope to aw
+// (trajopt.py:601-635; pyaw = d(sphere xy)/d(block yaw)). (A packed f32x2 form, two placed
+// spheres per instruction as in the fixed-obstacle pass, measured slower: blocks have 1-4
+// spheres, so the pair loop rarely runs and its reductions and registers cost more.)
+template <typename R>
+__device__ __forceinline__ void placed_pass(const R* pl, const R* pyaw, const R* br, R cx, R cy, R cz, R rr, int q0,
+                                            int q1, bool quad, R& v, R& ax, R& ay, R& az, R& aw) {
+  int q = q0;
+  for (; q < q1; ++q) {
+    const R dx = cx - pl[3 * q], dy = cy - pl[3 * q + 1], dz = cz - pl[3 * q + 2];
+    R sl;
+    v += pen_term(dx, dy, dz, rr + br[q], quad, &sl);
+    const R fx = sl * dx, fy = sl * dy, fz = sl * dz;
+    ax += fx;
+    ay += fy;
+    az += fz;
+    aw += fx * pyaw[2 * q] + fy * pyaw[2 * q + 1];
+  }
+}
+
 // Per-step state a waypoint tile carries across the phases (registers).
 template <typename R>
 struct WpState {
@@ -350,7 +380,7 @@ __device__ __forceinline__ void al_eval(AlCtx<R>& C, const typename TwinSceneOf<
   const bool interior = C.g_interior;
   const int h0 = C.g_h0, nh = C.g_nh, f0 = C.g_f0, f1 = C.g_f1;
   const R w_start = R(prm.w_start);
-  const int bar_count = C.L.NW + 32;
+  const int bar_count = C.L.NW + 32 * C.L.NA;
   WpState<R> st;
   R obj_w = R(0), carm = R(0), cblk = R(0);
 
@@ -364,7 +394,8 @@ __device__ __forceinline__ void al_eval(AlCtx<R>& C, const typename TwinSceneOf<
       // itself (4 tiles of 8 lanes, uniform trip count) so no tile waits for another warp's
       // FK; identical frames to the waypoint tiles' (same code, same operands)
       const int sub = lane >> 3;
-      for (int base = 0; base < B; base += 4) {
+      const int aux_id = (tid - C.L.NW) >> 5;  // second aux warp (NA = 2): blocks 4-7
+      for (int base = 4 * aux_id; base < B; base += 4 * C.L.NA) {
         const int bb = base + sub;
         const bool act = bb < B;
         const int wf = (act ? bb : 0) * T + T - 1;
@@ -390,11 +421,20 @@ __device__ __forceinline__ void al_eval(AlCtx<R>& C, const typename TwinSceneOf<
             C.pl[3 * q + 0] = f.ee[0] + c * ux - s * uy;
             C.pl[3 * q + 1] = f.ee[1] + s * ux + c * uy;
             C.pl[3 * q + 2] = f.ee[2] + uz;
+            // d(block sphere q)/d(placed yaw) (trajopt.py:601-635), once per step here
+            // instead of in every (item, sphere) pair of the placed-block pass
+            C.pyaw[2 * q + 0] = -s * ux - c * uy;
+            C.pyaw[2 * q + 1] = c * ux - s * uy;
           }
         }
       }
       __syncwarp();
+      if (C.L.NA == 2) {  // the twin below reads every block's pose: meet the second aux warp
+        if (aux_id == 1) bar_aux_arrive();
+        else bar_aux_sync();
+      }
       bar_placed_arrive(bar_count);
+      if (aux_id == 1) goto aux_done;  // the second aux warp only places blocks 4-7
       if (C.prof.on && lane == 0) atomicAdd(&g_al_arrive[1][5], (unsigned long long)(clock64() - C.prof.t));
       R cpl = twin_warp<R, KIND, SPB>(tw, C.rows, C.gpose, C.scr, lane, want_grad, pquad);
       if (C.prof.on && lane == 0) atomicAdd(&g_al_arrive[1][6], (unsigned long long)(clock64() - C.prof.t));
@@ -409,6 +449,7 @@ __device__ __forceinline__ void al_eval(AlCtx<R>& C, const typename TwinSceneOf<
       }
       if (lane == 0) C.scal[kCplace] = cpl;
     }
+  aux_done:;
   } else {
     // ================= phase A, waypoint tiles ============================================
     // ---- P1: tile FK, sphere centres
@@ -519,7 +560,6 @@ __device__ __forceinline__ void al_eval(AlCtx<R>& C, const typename TwinSceneOf<
         const bool act = is_wp && jb < b;
         R A[4] = {R(0), R(0), R(0), R(0)}, H[4] = {R(0), R(0), R(0), R(0)};
         if (act) {
-          const R cj = C.cp[jb], sj = C.sp[jb];
           const int q0 = sc.blk_start[jb], q1 = sc.blk_start[jb + 1];
 #pragma unroll
           for (int k = 0; k < kAlItems; ++k) {
@@ -531,17 +571,7 @@ __device__ __forceinline__ void al_eval(AlCtx<R>& C, const typename TwinSceneOf<
             const R cx = c[0], cy = c[1], cz = c[2];
             const R rr = arm ? ch.arm_r[si] : sc.br[h0 + si];
             R v = R(0), ax = R(0), ay = R(0), az = R(0), aw = R(0);
-            for (int q = q0; q < q1; ++q) {
-              const R dx = cx - C.pl[3 * q], dy = cy - C.pl[3 * q + 1], dz = cz - C.pl[3 * q + 2];
-              R sl;
-              v += pen_term(dx, dy, dz, rr + sc.br[q], quad, &sl);
-              const R fx = sl * dx, fy = sl * dy, fz = sl * dz;
-              ax += fx;
-              ay += fy;
-              az += fz;
-              // d(block sphere q)/d(placed yaw) (trajopt.py:601-635)
-              aw += fx * (-sj * sc.bu[q][0] - cj * sc.bu[q][1]) + fy * (cj * sc.bu[q][0] - sj * sc.bu[q][1]);
-            }
+            placed_pass(C.pl, C.pyaw, sc.br, cx, cy, cz, rr, q0, q1, quad, v, ax, ay, az, aw);
             gi[k][0] -= ax;
             gi[k][1] -= ay;
             gi[k][2] -= az;
@@ -766,10 +796,10 @@ __device__ __forceinline__ void al_validate(AlCtx<R>& C, const typename TwinScen
   // sizes from the kernel-parameter layout (uniform to the compiler; equal to the scene's)
   const int W = C.L.W, J = C.L.J, T = prm.T, B = C.L.B, S = C.L.S, SBn = C.L.SB;
   const bool manip = sc.manip != 0;
-  const bool is_aux = tid >= C.L.NW;
+  const bool is_aux = tid >= C.L.NW && tid < C.L.NW + 32;  // the first aux warp (a second one idles)
   const int lane = tid & 31;
   const int w = tid >> 3;
-  const bool is_wp = !is_aux && w < W;
+  const bool is_wp = tid < C.L.NW && w < W;
   const int j = tid & 7;
   const int b = is_wp ? w / T : 0;
   const int t = is_wp ? w - b * T : 0;
