@@ -90,7 +90,7 @@ __host__ __device__ inline AlLayout al_layout(int B, int T, int J, int S, int SB
   L.hp = take(3 * (SB > 0 ? SB : 1) * W * r);
   L.gh = take(3 * (SB > 0 ? SB : 1) * W * r);
   L.pg = take(8 * B * W * r);
-  L.pl = take(3 * (NB > 0 ? NB : 1) * r);
+  L.pl = take(4 * (NB > 0 ? NB : 1) * r);  // placed block spheres (x, y, z, radius)
   L.pyaw = take(2 * (NB > 0 ? NB : 1) * r);  // d(placed sphere xy)/d(block yaw)
   L.seg = take(3 * B * r);  // psi | cp | sp
   L.rows = take(4 * B * r);
@@ -269,20 +269,26 @@ __device__ __forceinline__ float pens_fixed_all_f2(const TrajScene<float>& sc, c
   PenAcc2 a;
   a.v = a.gx = a.gy = a.gz = f2_dup(0.f);
   const int ns = sc.n_static;
+  const float4* st = reinterpret_cast<const float4*>(sc.st4);  // (x, y, z, r): one LDS.128 each
+  const float4* sg = reinterpret_cast<const float4*>(sc.staged4);
   int o = 0;
 #pragma unroll 2
-  for (; o + 1 < ns; o += 2)
-    a = pen_two(a, cx, cy, cz, r, quad, sc.st_c[o][0], sc.st_c[o][1], sc.st_c[o][2], sc.st_r[o], sc.st_c[o + 1][0],
-                sc.st_c[o + 1][1], sc.st_c[o + 1][2], sc.st_r[o + 1]);
-  if (o < ns)
-    a = pen_two(a, cx, cy, cz, r, quad, sc.st_c[o][0], sc.st_c[o][1], sc.st_c[o][2], sc.st_r[o], c[0], c[1], c[2],
-                0.f);
-  for (o = f0; o + 1 < f1; o += 2)
-    a = pen_two(a, cx, cy, cz, r, quad, sc.staged[o][0], sc.staged[o][1], sc.staged[o][2], sc.br[o],
-                sc.staged[o + 1][0], sc.staged[o + 1][1], sc.staged[o + 1][2], sc.br[o + 1]);
-  if (o < f1)
-    a = pen_two(a, cx, cy, cz, r, quad, sc.staged[o][0], sc.staged[o][1], sc.staged[o][2], sc.br[o], c[0], c[1], c[2],
-                0.f);
+  for (; o + 1 < ns; o += 2) {
+    const float4 A = st[o], B = st[o + 1];
+    a = pen_two(a, cx, cy, cz, r, quad, A.x, A.y, A.z, A.w, B.x, B.y, B.z, B.w);
+  }
+  if (o < ns) {
+    const float4 A = st[o];
+    a = pen_two(a, cx, cy, cz, r, quad, A.x, A.y, A.z, A.w, c[0], c[1], c[2], 0.f);
+  }
+  for (o = f0; o + 1 < f1; o += 2) {
+    const float4 A = sg[o], B = sg[o + 1];
+    a = pen_two(a, cx, cy, cz, r, quad, A.x, A.y, A.z, A.w, B.x, B.y, B.z, B.w);
+  }
+  if (o < f1) {
+    const float4 A = sg[o];
+    a = pen_two(a, cx, cy, cz, r, quad, A.x, A.y, A.z, A.w, c[0], c[1], c[2], 0.f);
+  }
   float v0, v1, x0, x1, y0, y1, z0, z1;
   f2_split(a.v, v0, v1);
   f2_split(a.gx, x0, x1);
@@ -332,18 +338,26 @@ __device__ __forceinline__ R pens_fixed_all(const TrajScene<R>& sc, const R* c, 
 // spheres per instruction as in the fixed-obstacle pass, measured slower: blocks have 1-4
 // spheres, so the pair loop rarely runs and its reductions and registers cost more.)
 template <typename R>
-__device__ __forceinline__ void placed_pass(const R* pl, const R* pyaw, const R* br, R cx, R cy, R cz, R rr, int q0,
+__device__ __forceinline__ void placed_pass(const R* pl, const R* pyaw, R cx, R cy, R cz, R rr, int q0,
                                             int q1, bool quad, R& v, R& ax, R& ay, R& az, R& aw) {
-  int q = q0;
-  for (; q < q1; ++q) {
-    const R dx = cx - pl[3 * q], dy = cy - pl[3 * q + 1], dz = cz - pl[3 * q + 2];
+  for (int q = q0; q < q1; ++q) {
+    R px, py, pz, pr, wx, wy;
+    if constexpr (sizeof(R) == 4) {  // one LDS.128 + one LDS.64 per placed sphere
+      const float4 P = reinterpret_cast<const float4*>(pl)[q];
+      const float2 Y = reinterpret_cast<const float2*>(pyaw)[q];
+      px = P.x, py = P.y, pz = P.z, pr = P.w, wx = Y.x, wy = Y.y;
+    } else {
+      px = pl[4 * q], py = pl[4 * q + 1], pz = pl[4 * q + 2], pr = pl[4 * q + 3];
+      wx = pyaw[2 * q], wy = pyaw[2 * q + 1];
+    }
+    const R dx = cx - px, dy = cy - py, dz = cz - pz;
     R sl;
-    v += pen_term(dx, dy, dz, rr + br[q], quad, &sl);
+    v += pen_term(dx, dy, dz, rr + pr, quad, &sl);
     const R fx = sl * dx, fy = sl * dy, fz = sl * dz;
     ax += fx;
     ay += fy;
     az += fz;
-    aw += fx * pyaw[2 * q] + fy * pyaw[2 * q + 1];
+    aw += fx * wx + fy * wy;
   }
 }
 
@@ -418,9 +432,10 @@ __device__ __forceinline__ void al_eval(AlCtx<R>& C, const typename TwinSceneOf<
           }
           for (int q = sc.blk_start[bb] + j; q < sc.blk_start[bb + 1]; q += kTile) {
             const R ux = sc.bu[q][0], uy = sc.bu[q][1], uz = sc.bu[q][2];
-            C.pl[3 * q + 0] = f.ee[0] + c * ux - s * uy;
-            C.pl[3 * q + 1] = f.ee[1] + s * ux + c * uy;
-            C.pl[3 * q + 2] = f.ee[2] + uz;
+            C.pl[4 * q + 0] = f.ee[0] + c * ux - s * uy;
+            C.pl[4 * q + 1] = f.ee[1] + s * ux + c * uy;
+            C.pl[4 * q + 2] = f.ee[2] + uz;
+            C.pl[4 * q + 3] = sc.br[q];
             // d(block sphere q)/d(placed yaw) (trajopt.py:601-635), once per step here
             // instead of in every (item, sphere) pair of the placed-block pass
             C.pyaw[2 * q + 0] = -s * ux - c * uy;
@@ -571,7 +586,7 @@ __device__ __forceinline__ void al_eval(AlCtx<R>& C, const typename TwinSceneOf<
             const R cx = c[0], cy = c[1], cz = c[2];
             const R rr = arm ? ch.arm_r[si] : sc.br[h0 + si];
             R v = R(0), ax = R(0), ay = R(0), az = R(0), aw = R(0);
-            placed_pass(C.pl, C.pyaw, sc.br, cx, cy, cz, rr, q0, q1, quad, v, ax, ay, az, aw);
+            placed_pass(C.pl, C.pyaw, cx, cy, cz, rr, q0, q1, quad, v, ax, ay, az, aw);
             gi[k][0] -= ax;
             gi[k][1] -= ay;
             gi[k][2] -= az;
@@ -819,9 +834,10 @@ __device__ __forceinline__ void al_validate(AlCtx<R>& C, const typename TwinScen
     C.rows[4 * bb + 3] = yaw;
     for (int q = sc.blk_start[bb]; q < sc.blk_start[bb + 1]; ++q) {
       const R lx = sc.bu[q][0] + ox, ly = sc.bu[q][1] + oy, lz = sc.bu[q][2] + oz;
-      C.pl[3 * q + 0] = (lx * c - ly * s) + px;
-      C.pl[3 * q + 1] = (lx * s + ly * c) + py;
-      C.pl[3 * q + 2] = lz + pz;
+      C.pl[4 * q + 0] = (lx * c - ly * s) + px;
+      C.pl[4 * q + 1] = (lx * s + ly * c) + py;
+      C.pl[4 * q + 2] = lz + pz;
+      C.pl[4 * q + 3] = sc.br[q];
     }
   }
   __syncthreads();
@@ -859,7 +875,7 @@ __device__ __forceinline__ void al_validate(AlCtx<R>& C, const typename TwinScen
           worst = fmax(worst, (r + sc.br[o]) - Math<R>::sqrt_((dx * dx + dy * dy) + dz * dz));
         }
         for (int o = 0; o < p_end; ++o) {
-          const R dx = c[0] - C.pl[3 * o], dy = c[1] - C.pl[3 * o + 1], dz = c[2] - C.pl[3 * o + 2];
+          const R dx = c[0] - C.pl[4 * o], dy = c[1] - C.pl[4 * o + 1], dz = c[2] - C.pl[4 * o + 2];
           worst = fmax(worst, (r + sc.br[o]) - Math<R>::sqrt_((dx * dx + dy * dy) + dz * dz));
         }
       };

@@ -56,6 +56,10 @@ struct alignas(16) TrajScene {
   R staged[kMaxBlkS][3];          // block spheres at their staged (initial) poses
   R st_c[kMaxStat2][3];
   R st_r[kMaxStat2];
+  // packed copies (x, y, z, radius) of st_c / st_r and staged / br for the fp32 hot loops:
+  // one 16-byte shared-memory load per obstacle instead of four
+  alignas(16) R st4[kMaxStat2][4];
+  alignas(16) R staged4[kMaxBlkS][4];
   R pick_pos[kMaxSeg][3];         // grasp targets over the staged poses
   R pick_yaw[kMaxSeg];
   double pick_pos64[kMaxSeg][3];

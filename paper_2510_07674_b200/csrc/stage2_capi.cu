@@ -84,8 +84,8 @@ static void fill_scene(TrajScene<R>& s, const spasm_chain& ch, const spasm_traj_
   s.n_static = d.n_static;
   s.free_rows = d.rows_have_yaw;
   for (int o = 0; o < d.n_static; ++o) {
-    for (int k = 0; k < 3; ++k) s.st_c[o][k] = (R)d.static_centers[3 * o + k];
-    s.st_r[o] = (R)d.static_radii[o];
+    for (int k = 0; k < 3; ++k) s.st_c[o][k] = s.st4[o][k] = (R)d.static_centers[3 * o + k];
+    s.st_r[o] = s.st4[o][3] = (R)d.static_radii[o];
   }
   if (d.manipulation) {
     int q = 0;
@@ -100,9 +100,9 @@ static void fill_scene(TrajScene<R>& s, const spasm_chain& ch, const spasm_traj_
     for (int i = 0; i < q; ++i) {
       for (int k = 0; k < 3; ++k) {
         s.bu[i][k] = (R)(d.block_centers[3 * i + k] - d.grasp_offset[k]);
-        s.staged[i][k] = (R)staged_world[3 * i + k];
+        s.staged[i][k] = s.staged4[i][k] = (R)staged_world[3 * i + k];
       }
-      s.br[i] = (R)d.block_radii[i];
+      s.br[i] = s.staged4[i][3] = (R)d.block_radii[i];
     }
     for (int b = 0; b < d.n_blocks; ++b) {
       for (int k = 0; k < 3; ++k) {
