@@ -263,31 +263,46 @@ __device__ __forceinline__ PenAcc2 pen_two(PenAcc2 a, F2 cx, F2 cy, F2 cz, float
   return a;
 }
 
-__device__ __forceinline__ float pens_fixed_all_f2(const TrajScene<float>& sc, const float* c, float r, int f0,
-                                                   int f1, bool quad, float* g) {
+// pen_two with the obstacle pair already packed (PX = (ax, bx), ...)
+__device__ __forceinline__ PenAcc2 pen_two_packed(PenAcc2 a, F2 cx, F2 cy, F2 cz, float r, bool quad, F2 PX, F2 PY,
+                                                  F2 PZ, float ar, float br) {
+  const F2 dx = f2_sub(cx, PX), dy = f2_sub(cy, PY), dz = f2_sub(cz, PZ);
+  const F2 d2 = f2_fma(dz, dz, f2_fma(dy, dy, f2_mul(dx, dx)));
+  float d2a, d2b;
+  f2_split(d2, d2a, d2b);
+  const float ia = rsqrtf(d2a), ib = rsqrtf(d2b);
+  const F2 pen = f2_sub(f2_make(r + ar, r + br), f2_mul(d2, f2_make(ia, ib)));
+  float pa, pb;
+  f2_split(pen, pa, pb);
+  const bool la = pa > 0.f, lb = pb > 0.f;
+  pa = la ? pa : 0.f;
+  pb = lb ? pb : 0.f;
+  const float sa = la ? (quad ? 2.f * pa * ia : ia) : 0.f, sb = lb ? (quad ? 2.f * pb * ib : ib) : 0.f;
+  const F2 P = f2_make(pa, pb), SL = f2_make(-sa, -sb);
+  a.v = quad ? f2_fma(P, P, a.v) : f2_add(a.v, P);
+  a.gx = f2_fma(SL, dx, a.gx);
+  a.gy = f2_fma(SL, dy, a.gy);
+  a.gz = f2_fma(SL, dz, a.gz);
+  return a;
+}
+
+// fp32: the segment's packed obstacle list (TrajScene::obsp), kObsGroup independent pair
+// chains per iteration (the loop branch stops chains overlapping across iterations)
+__device__ __forceinline__ float pens_fixed_all_f2(const TrajScene<float>& sc, const float* c, float r, int b,
+                                                   bool quad, float* g) {
   const F2 cx = f2_dup(c[0]), cy = f2_dup(c[1]), cz = f2_dup(c[2]);
   PenAcc2 a;
   a.v = a.gx = a.gy = a.gz = f2_dup(0.f);
-  const int ns = sc.n_static;
-  const float4* st = reinterpret_cast<const float4*>(sc.st4);  // (x, y, z, r): one LDS.128 each
-  const float4* sg = reinterpret_cast<const float4*>(sc.staged4);
-  int o = 0;
-#pragma unroll 2
-  for (; o + 1 < ns; o += 2) {
-    const float4 A = st[o], B = st[o + 1];
-    a = pen_two(a, cx, cy, cz, r, quad, A.x, A.y, A.z, A.w, B.x, B.y, B.z, B.w);
-  }
-  if (o < ns) {
-    const float4 A = st[o];
-    a = pen_two(a, cx, cy, cz, r, quad, A.x, A.y, A.z, A.w, c[0], c[1], c[2], 0.f);
-  }
-  for (o = f0; o + 1 < f1; o += 2) {
-    const float4 A = sg[o], B = sg[o + 1];
-    a = pen_two(a, cx, cy, cz, r, quad, A.x, A.y, A.z, A.w, B.x, B.y, B.z, B.w);
-  }
-  if (o < f1) {
-    const float4 A = sg[o];
-    a = pen_two(a, cx, cy, cz, r, quad, A.x, A.y, A.z, A.w, c[0], c[1], c[2], 0.f);
+  const ulonglong2* sp = reinterpret_cast<const ulonglong2*>(sc.obsp[b]);
+  const int np = sc.obs_np[b];
+  for (int p0 = 0; p0 < np; p0 += kObsGroup) {
+#pragma unroll
+    for (int u = 0; u < kObsGroup; ++u) {
+      const ulonglong2 XY = sp[2 * (p0 + u)], ZR = sp[2 * (p0 + u) + 1];
+      float ra, rb;
+      f2_split(F2{ZR.y}, ra, rb);
+      a = pen_two_packed(a, cx, cy, cz, r, quad, F2{XY.x}, F2{XY.y}, F2{ZR.x}, ra, rb);
+    }
   }
   float v0, v1, x0, x1, y0, y1, z0, z1;
   f2_split(a.v, v0, v1);
@@ -303,9 +318,9 @@ __device__ __forceinline__ float pens_fixed_all_f2(const TrajScene<float>& sc, c
 // One sphere against every fixed obstacle (statics, then staged spheres [f0, f1)), on one
 // lane: returns the summed value and adds the unscaled gradient to g.
 template <typename R>
-__device__ __forceinline__ R pens_fixed_all(const TrajScene<R>& sc, const R* c, R r, int f0, int f1, bool quad,
+__device__ __forceinline__ R pens_fixed_all(const TrajScene<R>& sc, const R* c, R r, int b, int f0, int f1, bool quad,
                                             R* g) {
-  if constexpr (sizeof(R) == 4) return pens_fixed_all_f2(sc, c, r, f0, f1, quad, g);
+  if constexpr (sizeof(R) == 4) return pens_fixed_all_f2(sc, c, r, b, quad, g);
   const R cx = c[0], cy = c[1], cz = c[2];
   R v = R(0), gx = R(0), gy = R(0), gz = R(0);
 #pragma unroll 4
@@ -544,7 +559,7 @@ __device__ __forceinline__ void al_eval(AlCtx<R>& C, const typename TwinSceneOf<
         const int s = arm ? it : it - S;
         const R* c = arm ? C.armw + (w * S + s) * 3 : C.hp + (w * SBn + s) * 3;
         R gg[3] = {R(0), R(0), R(0)};
-        const R v = pens_fixed_all(sc, c, arm ? ch.arm_r[s] : sc.br[h0 + s], f0, f1, quad, gg);
+        const R v = pens_fixed_all(sc, c, arm ? ch.arm_r[s] : sc.br[h0 + s], b, f0, f1, quad, gg);
         R* go = arm ? C.ga + (w * S + s) * 3 : C.gh + (w * SBn + s) * 3;
         go[0] = gg[0];
         go[1] = gg[1];

@@ -22,6 +22,8 @@ constexpr int kMaxStat2 = 128;    // static obstacle spheres
 constexpr int kIkRestarts = 16;   // ik_solve_batch default restarts (robot.py:230)
 constexpr double kIkPosTol = 1e-4, kIkYawTol = 1e-3, kIkDamping = 1e-3;  // robot.py:22-24
 constexpr int kPolishMaxIters = 1000;                                     // trajopt.py:100
+constexpr int kObsGroup = 4;                                               // obstacle pairs per pass iteration
+constexpr int kObsPairs = ((128 + 64) / 2 + kObsGroup - 1) / kObsGroup * kObsGroup;  // statics + staged, padded
 
 template <typename R>
 struct alignas(16) ChainDesc {
@@ -60,6 +62,12 @@ struct alignas(16) TrajScene {
   // one 16-byte shared-memory load per obstacle instead of four
   alignas(16) R st4[kMaxStat2][4];
   alignas(16) R staged4[kMaxBlkS][4];
+  // fp32 fixed-obstacle lists per segment b (the statics, then the staged spheres of blocks
+  // > b), two by two in packed-pair order (x0 x1 y0 y1 z0 z1 r0 r1) so two 16-byte loads
+  // give the f32x2 operands of a pair, padded with far dummies (inactive) to whole groups of
+  // kObsGroup pairs: the pass then runs kObsGroup independent pair chains per iteration
+  alignas(16) R obsp[sizeof(R) == 4 ? kMaxSeg : 1][kObsPairs][8];
+  int obs_np[kMaxSeg];            // pairs in obsp[b], a multiple of kObsGroup
   R pick_pos[kMaxSeg][3];         // grasp targets over the staged poses
   R pick_yaw[kMaxSeg];
   double pick_pos64[kMaxSeg][3];

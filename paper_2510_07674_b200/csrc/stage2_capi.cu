@@ -118,6 +118,29 @@ static void fill_scene(TrajScene<R>& s, const spasm_chain& ch, const spasm_traj_
       s.goal[j] = (R)d.goal[j];
     }
   }
+  // fp32 fixed-obstacle lists per segment (stage2.cuh obsp): statics, then the staged spheres
+  // of the later blocks, padded with far inactive dummies to whole kObsGroup-pair groups
+  if constexpr (sizeof(R) == 4) {
+    for (int b = 0; b < s.B; ++b) {
+      const int f0 = s.manip ? s.blk_start[b + 1] : 0, f1 = s.manip ? s.n_blk : 0;
+      const int n = s.n_static + (f1 - f0);
+      const int np = (n + 2 * kObsGroup - 1) / (2 * kObsGroup) * kObsGroup;
+      s.obs_np[b] = np;
+      for (int o = 0; o < 2 * np; ++o) {
+        R c[3] = {(R)1e18, (R)1e18, (R)1e18}, r = (R)0;
+        if (o < s.n_static) {
+          for (int k = 0; k < 3; ++k) c[k] = s.st_c[o][k];
+          r = s.st_r[o];
+        } else if (o < n) {
+          const int q = f0 + (o - s.n_static);
+          for (int k = 0; k < 3; ++k) c[k] = s.staged[q][k];
+          r = s.br[q];
+        }
+        for (int k = 0; k < 3; ++k) s.obsp[b][o / 2][2 * k + (o & 1)] = c[k];
+        s.obsp[b][o / 2][6 + (o & 1)] = r;
+      }
+    }
+  }
 }
 
 static inline cudaStream_t as_stream2(void* s) { return reinterpret_cast<cudaStream_t>(s); }
