@@ -641,39 +641,65 @@ __device__ __forceinline__ void al_eval(AlCtx<R>& C, const typename TwinSceneOf<
     __syncwarp();  // the J^T products below read sphere gradients other lanes of the tile own
     if (want_grad) {
       // arm: suffix sums over links >= k of (g, a x g), lane k = joint k (trajopt.py:586-590)
-      R G[3] = {R(0), R(0), R(0)}, Mv[3] = {R(0), R(0), R(0)};
-      if (is_wp && j < J) {
-        for (int s = C.g_slo; s < C.g_shi; ++s) {
-          const R* a = C.armw + (w * S + s) * 3;
-          const R* gg = C.ga + (w * S + s) * 3;
-          R m[3];
-          cross3(a, gg, m);
-          G[0] += gg[0];
-          G[1] += gg[1];
-          G[2] += gg[2];
-          Mv[0] += m[0];
-          Mv[1] += m[1];
-          Mv[2] += m[2];
+      // the link's first sphere by selects (no divergent branch: every lane of the warp runs
+      // it), further spheres of multi-sphere links in the loop
+      R G[3], Mv[3];
+      const int wq = is_wp ? w : 0;
+      {
+        const bool ok = is_wp && C.g_slo < C.g_shi;
+        const int s0 = ok ? C.g_slo : 0;
+        const R* a = C.armw + (wq * S + s0) * 3;
+        const R* gg = C.ga + (wq * S + s0) * 3;
+        R m[3];
+        cross3(a, gg, m);
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          G[c] = ok ? R(0) + gg[c] : R(0);
+          Mv[c] = ok ? R(0) + m[c] : R(0);
         }
+      }
+      for (int s = C.g_slo + 1; s < C.g_shi; ++s) {
+        const R* a = C.armw + (w * S + s) * 3;
+        const R* gg = C.ga + (w * S + s) * 3;
+        R m[3];
+        cross3(a, gg, m);
+        G[0] += gg[0];
+        G[1] += gg[1];
+        G[2] += gg[2];
+        Mv[0] += m[0];
+        Mv[1] += m[1];
+        Mv[2] += m[2];
       }
 #pragma unroll
       for (int d = 1; d < kTile; d <<= 1) {
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
           const R gv = tlw.down(G[c], d), mv = tlw.down(Mv[c], d);
-          if (j + d < kTile) {
-            G[c] += gv;
-            Mv[c] += mv;
-          }
+          const bool in = j + d < kTile;
+          G[c] = in ? G[c] + gv : G[c];
+          Mv[c] = in ? Mv[c] + mv : Mv[c];
         }
       }
       R og[3];
       cross3(st.o, G, og);
       st.garm = (st.z[0] * (Mv[0] - og[0]) + st.z[1] * (Mv[1] - og[1])) + st.z[2] * (Mv[2] - og[2]);
       // held block: every joint moves it (trajopt.py:592-599)
-      R Gh[3] = {R(0), R(0), R(0)}, Mh[3] = {R(0), R(0), R(0)};
+      R Gh[3], Mh[3];
+      {  // the lane's first held sphere by selects, more (blocks of > 8 spheres) in the loop
+        const bool ok = interior && is_wp && j < nh;
+        const int s0 = ok ? j : 0;
+        const R* a = C.hp + (wq * SBn + s0) * 3;
+        const R* gg = C.gh + (wq * SBn + s0) * 3;
+        R m[3];
+        cross3(a, gg, m);
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          Gh[c] = ok ? R(0) + gg[c] : R(0);
+          Mh[c] = ok ? R(0) + m[c] : R(0);
+        }
+      }
       if (interior && is_wp) {
-        for (int s = j; s < nh; s += kTile) {
+        for (int s = j + kTile; s < nh; s += kTile) {
           const R* a = C.hp + (w * SBn + s) * 3;
           const R* gg = C.gh + (w * SBn + s) * 3;
           R m[3];
