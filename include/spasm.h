@@ -373,6 +373,11 @@ int spasm_al_profile_warps(double* out);
  * enable 1/0; out (8 doubles, optional) receives and resets them. */
 int spasm_ik_profile(int enable, double* out);
 
+/* Self-test of the fp32 branch-free math on the device (n pseudo-random inputs from seed):
+ * counts[0] = bit mismatches of the branch-free atan2 against atan2f, counts[1] / [2] = of
+ * the normalize_yaw / np.mod fast-range folds against the scalar routines. All 0 expected. */
+int spasm_selftest_math(int64_t n, uint64_t seed, int64_t counts[3]);
+
 #ifdef __cplusplus
 }
 #endif

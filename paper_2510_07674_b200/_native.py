@@ -153,6 +153,7 @@ SIGNATURES = {
     "spasm_al_profile": (c_int, [c_int, c_void_p]),
     "spasm_al_profile_warps": (c_int, [c_void_p]),
     "spasm_ik_profile": (c_int, [c_int, c_void_p]),
+    "spasm_selftest_math": (c_int, [c_int64, c_uint64, c_void_p]),
     "spasm_tetris_model_create": (
         c_int,
         [POINTER(c_void_p), c_int, c_void_p, c_void_p, c_void_p, c_int, c_void_p, c_void_p, c_void_p,
