@@ -588,6 +588,9 @@ __device__ __forceinline__ void al_eval(AlCtx<R>& C, const typename TwinSceneOf<
       for (int k = 0; k < kAlItems; ++k) gi[k][0] = gi[k][1] = gi[k][2] = R(0);
       for (int jb = 0; jb + 1 < B; ++jb) {
         const bool act = is_wp && jb < b;
+        // a warp whose tiles all sit in segments <= jb has nothing here (its reduce-scatter
+        // would sum zeros it does not store): skip the block, warp-uniformly
+        if (!__any_sync(0xffffffffu, act)) continue;
         R A[4] = {R(0), R(0), R(0), R(0)}, H[4] = {R(0), R(0), R(0), R(0)};
         if (act) {
           const int q0 = sc.blk_start[jb], q1 = sc.blk_start[jb + 1];
