@@ -374,7 +374,8 @@ struct PolishRun {
 // The whole polish of one configuration. Optional speculative mode (k_ik_group): `best`
 // points at a shared slot that becomes the winning tile's index once every restart has
 // finished IK; a tile whose index `me` lost stops polishing (its result is discarded, so
-// the winner's result is unchanged).
+// the winner's result is unchanged). The slots are polled one step ahead of their test, so a
+// losing tile may run one step more than necessary.
 template <typename R>
 __device__ bool tile_polish(const Tile& tl, const ChainDesc<R>& ch, R& q_io, const R tp[3], R ty,
                             const volatile int* best = nullptr, int me = 0,
@@ -384,17 +385,21 @@ __device__ bool tile_polish(const Tile& tl, const ChainDesc<R>& ch, R& q_io, con
   R qj = q_io;  // iterate in a register (q_io may live in memory when this is not inlined)
   PolishRun<R> run;
   run.begin(tl, ch, qj);
+  int b_seen = -1;                 // the slots as of the last poll (this tile just led)
+  unsigned long long c_seen = mine;
   for (;;) {
     if (best) {  // abort once another tile is the winner or the current best candidate
       int stop = 0;
-      if (tl.j == 0) {
-        const int b = *best;
-        stop = (b >= 0) ? (b != me) : (cur != nullptr && *cur != mine);
-      }
+      if (tl.j == 0) stop = (b_seen >= 0) ? (b_seen != me) : (cur != nullptr && c_seen != mine);
       // any replica's lane 0 seeing the stop condition stops the whole tile / warp together
       if (tl.any(stop != 0)) {
         q_io = qj;
         return false;
+      }
+      // poll now, test after this step: the (possibly cluster-remote) loads overlap the step
+      if (tl.j == 0) {
+        b_seen = *best;
+        if (cur != nullptr) c_seen = *cur;
       }
     }
     if (run.step(tl, qj, tp, ty)) break;

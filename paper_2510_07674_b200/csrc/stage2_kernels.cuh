@@ -22,6 +22,8 @@
 // memory column-major ([field][w]) so every thread touches its own bank column. All
 // reductions run in a fixed order (no atomics): results are deterministic per seed.
 #pragma once
+#include <cooperative_groups.h>
+
 #include "al_tile.cuh"
 #include "coop.cuh"
 #include "seedseq.cuh"
@@ -35,6 +37,10 @@ namespace spasm {
 // [6] winners polished speculatively to completion, [7] restarts' IK iterations (sum)
 static __device__ unsigned long long g_ik_prof[8];
 static __device__ int g_ik_prof_on;
+
+// orders this thread's earlier shared-memory writes (own CTA or a cluster peer's) before its
+// later ones as seen from any CTA of the cluster
+__device__ __forceinline__ void cluster_fence() { asm volatile("fence.acq_rel.cluster;" ::: "memory"); }
 
 // ---------------------------------------------------------------------------------------
 // IK / lifting
@@ -72,21 +78,32 @@ __device__ __forceinline__ void lift_target(const TrajScene<R>& sc, const double
   *ty = (R)wrap_yaw<double>(yaw + (double)sc.grasp_yaw);
 }
 
-// one CTA per (draw, target) group; one 8-lane tile per seeded restart (lane = joint), each
-// tile in its own warp (lanes 8-31 idle) so that restarts in different phases (IK vs
-// speculative polish) never share a warp and serialise on divergence
-// MAXT = the block-size bound: 512 (<= 16 restarts) lets ptxas use 128 registers (the
-// per-iteration FK/DLS state spills under the 64-register cap of 1024-thread blocks); the
-// launcher takes it when the grid fits one CTA per SM.
+// one thread-block cluster of CS CTAs per (draw, target) group (CS = 1: a plain CTA); the
+// group's seeded restarts are dealt out rpc per CTA, one 8-lane tile per restart, each tile in
+// its own warp (lanes 8-31 idle) so that restarts in different phases (IK vs speculative
+// polish) never share a warp and serialise on divergence. Splitting a group over a cluster
+// spreads its warps over several SMs: an IK iteration issues ~110 warp-wide SHFLs and an SM
+// issues one per cycle (profiles/r02_microbench_shfl_lds_throughput.txt), so 16 restart
+// warps on one SM wait on each other's shuffles. The group's selection slots (keys, scores,
+// flags, the finished count, the speculation key and the winner) live in the shared memory
+// of the cluster's rank-0 CTA and are reached through distributed shared memory.
+// MAXT = the block-size bound: 512 (<= 16 restarts per CTA) lets ptxas use 128 registers (the
+// per-iteration FK/DLS state spills under the 64-register cap of 1024-thread blocks).
 template <typename R, int MAXT>
 __global__ void __launch_bounds__(MAXT) k_ik_group(const TrajScene<R>* __restrict__ g_scene, int n_targets, int n_draws,
                                                   uint64_t seed, uint64_t draw_stride, int restarts, int max_iters,
                                                   double damping, const double* __restrict__ tpos_in,
                                                   const double* __restrict__ tyaw_in, const double* __restrict__ rows,
                                                   int D, int polish, int score_statics, IkOut out,
-                                                  const int32_t* __restrict__ n_rows) {
+                                                  const int32_t* __restrict__ n_rows, int rpc) {
+  namespace cg = cooperative_groups;
+  cg::cluster_group cl = cg::this_cluster();
+  const int CS = (int)cl.num_blocks();
+  const int crank = (int)cl.block_rank();
+  const int grp = blockIdx.x / CS;
   // device row count (stage-1 result read in place): groups of absent rows exit at once
-  if (n_rows && (int)(blockIdx.x % n_targets) >= g_scene->B + *n_rows * g_scene->B) return;
+  // (uniform over the cluster: every CTA of it serves the same group)
+  if (n_rows && (int)(grp % n_targets) >= g_scene->B + *n_rows * g_scene->B) return;
   __shared__ ChainDesc<R> ch_s;
   __shared__ R s_key[32], s_score[32];
   __shared__ int s_ok[32];
@@ -95,7 +112,7 @@ __global__ void __launch_bounds__(MAXT) k_ik_group(const TrajScene<R>* __restric
   __shared__ int s_its[32];
   const bool prof = g_ik_prof_on != 0;
   const long long t_start = prof ? clock64() : 0;
-  if (threadIdx.x == 0) {
+  if (threadIdx.x == 0 && crank == 0) {
     s_best = -1;
     s_done = 0;
     s_cur = ~0ull;
@@ -106,15 +123,22 @@ __global__ void __launch_bounds__(MAXT) k_ik_group(const TrajScene<R>* __restric
     int4* dst = reinterpret_cast<int4*>(&ch_s);
     for (int i = threadIdx.x; i < (int)(sizeof(ChainDesc<R>) / sizeof(int4)); i += blockDim.x) dst[i] = src[i];
   }
-  __syncthreads();
+  cl.sync();  // rank 0's slots are initialised before any CTA of the cluster touches them
+  // the group's slots in rank 0 (generic pointers into distributed shared memory)
+  volatile R* const key_p = cl.map_shared_rank(s_key, 0);
+  volatile R* const score_p = cl.map_shared_rank(s_score, 0);
+  volatile int* const ok_p = cl.map_shared_rank(s_ok, 0);
+  volatile int* const its_p = cl.map_shared_rank(s_its, 0);
+  int* const best_p = cl.map_shared_rank(&s_best, 0);
+  int* const done_p = cl.map_shared_rank(&s_done, 0);
+  unsigned long long* const cur_p = cl.map_shared_rank(&s_cur, 0);
   const ChainDesc<R>& ch = ch_s;
-  const int grp = blockIdx.x;
   const int a = grp / n_targets, t = grp - a * n_targets;
   const int J = ch.J;
   // every lane of a restart's warp runs the tile (4 identical replicas of the 8-lane tile),
   // so its shuffles can name the whole warp (Tile::make_warp); lanes 0-7 write results
   const Tile tl = Tile::make_warp();
-  const int tile = threadIdx.x >> 5;
+  const int tile = crank * rpc + (int)(threadIdx.x >> 5);
   const bool tile_lane = (threadIdx.x & 31) < kTile;
   const bool lane0 = (threadIdx.x & 31) == 0;
   R tp[3], ty;
@@ -144,37 +168,37 @@ __global__ void __launch_bounds__(MAXT) k_ik_group(const TrajScene<R>* __restric
     R score;
     int its = 0;
     const bool ok = tile_ik<R>(tl, ch, qj, tp, ty, max_iters, R(damping), &score, &its);
-    if (prof && lane0) s_its[tile] = its;
+    if (prof && lane0) its_p[tile] = its;
     const R key = (ok ? R(0) : R(1e6)) + score;
     // speculation order: (fp32 image of the key, restart); the exact winner is s_best below
     const unsigned long long mine = ((unsigned long long)order_key((float)key) << 32) | (unsigned)tile;
     int last = 0, lead = 0;
     if (lane0) {
-      s_key[tile] = key;
-      s_score[tile] = score;
-      s_ok[tile] = ok;
-      __threadfence_block();
-      lead = atomicMin(&s_cur, mine) > mine;
-      last = atomicAdd(&s_done, 1) == restarts - 1;
+      key_p[tile] = key;
+      score_p[tile] = score;
+      ok_p[tile] = ok;
+      cluster_fence();
+      lead = atomicMin(cur_p, mine) > mine;
+      last = atomicAdd(done_p, 1) == restarts - 1;
     }
     last = __shfl_sync(0xffffffffu, last, 0);
     lead = __shfl_sync(0xffffffffu, lead, 0);
     if (last && lane0) {  // the last restart to finish picks the first minimum (np.argmin)
-      __threadfence_block();
+      cluster_fence();
       int b = 0;
       for (int r = 1; r < restarts; ++r)
-        if (((volatile R*)s_key)[r] < ((volatile R*)s_key)[b]) b = r;
-      *((volatile int*)&s_best) = b;
+        if (key_p[r] < key_p[b]) b = r;
+      *((volatile int*)best_p) = b;
       if (prof) {
         atomicAdd(&g_ik_prof[1], (unsigned long long)(clock64() - t_start));
         int mx = 0;
         unsigned long long sum = 0;
         for (int r = 0; r < restarts; ++r) {
-          mx = max(mx, ((volatile int*)s_its)[r]);
-          sum += ((volatile int*)s_its)[r];
+          mx = max(mx, its_p[r]);
+          sum += its_p[r];
         }
         atomicAdd(&g_ik_prof[3], (unsigned long long)mx);
-        atomicAdd(&g_ik_prof[4], (unsigned long long)((volatile int*)s_its)[b]);
+        atomicAdd(&g_ik_prof[4], (unsigned long long)its_p[b]);
         atomicAdd(&g_ik_prof[7], sum);
       }
     }
@@ -183,10 +207,18 @@ __global__ void __launch_bounds__(MAXT) k_ik_group(const TrajScene<R>* __restric
     // the winner's polish usually overlaps the slower restarts' IK iterations
     ik_q = qj;
     if (polish && __all_sync(0xffffffffu, lead != 0))
-      pol_spec = tile_polish<R>(tl, ch, qj, tp, ty, &s_best, tile, &s_cur, mine, &spec_done, &spec_its);
+      pol_spec = tile_polish<R>(tl, ch, qj, tp, ty, best_p, tile, cur_p, mine, &spec_done, &spec_its);
   }
-  __syncthreads();
-  if (!__all_sync(0xffffffffu, tile == s_best)) return;  // the whole winner warp stays: its polish shuffles warp-wide
+  cl.sync();  // every restart has finished IK and the winner is known
+  const int best = *((volatile int*)best_p);
+  int best_ok = 0;
+  R best_score = R(0);
+  if (tile == best) {
+    best_ok = ok_p[best];
+    best_score = score_p[best];
+  }
+  cl.sync();  // rank 0's slots are not read past this point (its CTA may exit)
+  if (!__all_sync(0xffffffffu, tile == best)) return;  // the whole winner warp stays: its polish shuffles warp-wide
   bool pol = true;
   R pen = R(0);
   if (polish) {
@@ -209,9 +241,9 @@ __global__ void __launch_bounds__(MAXT) k_ik_group(const TrajScene<R>* __restric
   if (!tile_lane) return;
   if (tl.j < J) reinterpret_cast<R*>(out.sol)[(int64_t)grp * J + tl.j] = qj;
   if (tl.j == 0) {
-    out.ik_ok[grp] = (uint8_t)s_ok[s_best];
+    out.ik_ok[grp] = (uint8_t)best_ok;
     if (out.pol_ok) out.pol_ok[grp] = (uint8_t)pol;
-    reinterpret_cast<R*>(out.score)[grp] = s_score[s_best];
+    reinterpret_cast<R*>(out.score)[grp] = best_score;
     if (out.pen) reinterpret_cast<R*>(out.pen)[grp] = pen;
   }
 }

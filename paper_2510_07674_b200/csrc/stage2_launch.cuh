@@ -162,17 +162,42 @@ int launch_ik(const Traj& tr, int n_targets, int n_draws, uint64_t seed, uint64_
   if (n_targets <= 0) return SPASM_OK;
   SPASM_REQUIRE(restarts >= 1 && restarts <= 32, "restarts must be in [1, 32]");
   const int64_t groups = (int64_t)n_targets * n_draws;
-  const int bs = restarts * 32;  // one warp per restart tile (k_ik_group)
-  const int64_t grid = groups;
-  if (bs <= 512 && grid <= kNumSMs)
-    k_ik_group<R, 512><<<(unsigned)grid, bs, 0, s>>>(tr.dev<R>(), n_targets, n_draws, seed, stride, restarts,
-                                                     max_iters, damping, tpos, tyaw, rows, D, polish, score_statics, out,
-                                                     n_rows);
+  // cluster size: spread each group's restart warps over CS CTAs (k_ik_group) so that the
+  // busiest SM carries the fewest restart warps, assuming the CTAs spread evenly over the
+  // SMs (CS in {1, 2, 4, 8}, the smallest on ties; 1 when the grid is too large to gain)
+  int cs = 1;
+  int64_t best_load = INT64_MAX;
+  for (int c = 1; c <= 8; c *= 2) {
+    const int rpc = (restarts + c - 1) / c;
+    if (c > restarts || groups * c > (int64_t)1 << 30) break;
+    const int64_t load = ((groups * c + kNumSMs - 1) / kNumSMs) * rpc;
+    if (load < best_load) {
+      best_load = load;
+      cs = c;
+    }
+  }
+  const int rpc = (restarts + cs - 1) / cs;
+  const int bs = rpc * 32;  // one warp per restart tile
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(groups * cs));
+  cfg.blockDim = dim3((unsigned)bs);
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = (unsigned)cs;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  // the 512-thread bound (128 registers) whenever a CTA holds at most 16 restarts and the
+  // CTAs fit the register file side by side; else the 1024-thread bound (64 registers)
+  const bool narrow = bs <= 512 && (bs <= 256 || groups * cs <= kNumSMs);
+  if (narrow)
+    SPASM_CUDA_TRY(cudaLaunchKernelEx(&cfg, k_ik_group<R, 512>, tr.dev<R>(), n_targets, n_draws, seed, stride, restarts,
+                                      max_iters, damping, tpos, tyaw, rows, D, polish, score_statics, out, n_rows, rpc));
   else
-    k_ik_group<R, 1024><<<(unsigned)grid, bs, 0, s>>>(tr.dev<R>(), n_targets, n_draws, seed, stride, restarts,
-                                                      max_iters, damping, tpos, tyaw, rows, D, polish, score_statics, out,
-                                                     n_rows);
-  SPASM_CHECK_LAUNCH();
+    SPASM_CUDA_TRY(cudaLaunchKernelEx(&cfg, k_ik_group<R, 1024>, tr.dev<R>(), n_targets, n_draws, seed, stride, restarts,
+                                      max_iters, damping, tpos, tyaw, rows, D, polish, score_statics, out, n_rows, rpc));
   return SPASM_OK;
 }
 
