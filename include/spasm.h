@@ -357,6 +357,11 @@ int spasm_al_records(const spasm_traj* traj, int dtype, int64_t P, const spasm_a
 int spasm_solve_al(const spasm_traj* traj, int dtype, const spasm_al_config* cfg, const void* values, int64_t P,
                    const int32_t* n_active, const int32_t* lift_status, void* workspace, int64_t workspace_bytes,
                    void* best_values, spasm_al_result* result, void* stream);
+/* Host copy of the last SPASM_OK spasm_solve_al's accepted trajectory as float64 (B,T,dof),
+ * n = B*T*dof values: staged in pinned memory by the solve's one D2H copy, so reading it
+ * needs no CUDA call (AlResult.trajectory, trajopt.py:1056-1063; the values
+ * _particle_trajectory turns into segments). SPASM_ERR_USAGE when nothing is staged. */
+int spasm_al_best_host(const spasm_traj* traj, double* out, int64_t n);
 
 /* Diagnostic: per-phase cycle counters of the fp32 AL kernel (marks 0-4: inner-step phases
  * P1-P5, 8: pick-waypoint polish, 9: re-evaluation + validate; 12-19 / 20-27: when thread

@@ -258,6 +258,7 @@ SIGNATURES = {
         [c_void_p, c_int, POINTER(spasm_al_config), c_void_p, c_int64, c_void_p, c_void_p, c_void_p, c_int64,
          c_void_p, POINTER(spasm_al_result), c_void_p],
     ),
+    "spasm_al_best_host": (c_int, [c_void_p, c_void_p, c_int64]),
 }
 
 _lib = None

@@ -135,33 +135,66 @@ __global__ void __launch_bounds__(kSortThreads) k_radix_scatter(const K* __restr
   }
 }
 
-// Small batches (n <= kSortCtaMax): every pass in ONE CTA of 1024 threads, chunks of 1024
-// keys scattered in order (match_any ranks + per-warp digit offsets), so the sort stays
-// stable and needs one launch instead of 3 per pass (the satisfying-particle ordering of
-// particle_opt.py:363 runs on m <= 8k keys every restart; above 8k the multi-CTA passes win).
-constexpr int kSortCtaMax = 8192;
+// Small batches (n <= kSortCtaMax): every pass in ONE CTA of 512 threads. Warp w owns the
+// contiguous segment [w * 32 * ITEMS, (w + 1) * 32 * ITEMS); lane l holds its positions seg + i * 32 + l (i < ITEMS: coalesced loads, batch i = 32
+// consecutive keys). Per 8-bit digit pass:
+//   1. per-warp digit counts cnt[w][d] (__match_any_sync peers; the batch's leader adds),
+//   2. one exclusive scan over the counters in digit-major order (d, w): warp w's keys of
+//      digit d land after every earlier warp's keys of digit d and every smaller digit,
+//   3. each warp walks its batches again in order; the leader of a digit group takes its
+//      base by a shared atomicAdd on cnt[w][d] (one warp's atomics on an address are
+//      performed in issue order, so batch i precedes batch i+1) and broadcasts it; key i of
+//      the group goes to base + its rank among the group,
+// so every pass is stable and ties keep their index order (numpy's kind="stable"). Three CTA
+// barriers per pass, against four per 1024-key chunk and a serial 32-warp prefix before
+// (the satisfying-particle ordering of particle_opt.py:363 runs on m <= 8k keys every restart).
+constexpr int kSortCtaThreads = 512;
+constexpr int kSortCtaWarps = kSortCtaThreads / 32;
+// Above 8k keys the multi-CTA passes win (spasm_sort_pairs, scripts/sort_timing.py on B200:
+// 16k keys 87 us in one CTA against 67 us over 8 CTAs; the one-CTA form at 2k / 4k / 8k keys
+// 24 / 34 / 50 us against 26 / 38 / 62 us for the previous chunked single-CTA sort)
+constexpr int kSortCtaMax = kSortCtaThreads * 16;  // 8192
+constexpr int kSortCntStride = 257;  // counter row stride: fewer bank conflicts in the digit-major scan
 
-template <typename K>
-__global__ void __launch_bounds__(1024) k_radix_sort_cta(K* __restrict__ ka, uint32_t* __restrict__ va,
-                                                         K* __restrict__ kb, uint32_t* __restrict__ vb, int n,
-                                                         int key_bits) {
-  __shared__ unsigned int run[256];
-  __shared__ unsigned int wcnt[32][256];
+template <typename K, int ITEMS>
+__global__ void __launch_bounds__(kSortCtaThreads) k_radix_sort_cta(K* ka, uint32_t* va, K* kb, uint32_t* vb, int n,
+                                                                    int key_bits) {
+  constexpr int NW = kSortCtaWarps, TPD = NW / 8;  // threads per digit in the scan (8 counters each)
+  constexpr int G = ITEMS < 16 ? ITEMS : 16;       // keys per lane loaded together by the scatter walk
+  __shared__ unsigned int cnt[NW * kSortCntStride];
+  __shared__ unsigned int wsum[32];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const unsigned lt_mask = (1u << lane) - 1u;
+  const int seg = warp * 32 * ITEMS + lane;
+  unsigned int* const row = cnt + warp * kSortCntStride;
   for (int shift = 0; shift < key_bits; shift += 8) {
-    if (tid < 256) run[tid] = 0;
-    for (int w = 0; w < 32; ++w)
-      if (tid < 256) wcnt[w][tid] = 0;
-    __syncthreads();
-    for (int i = tid; i < n; i += 1024) atomicAdd(&run[(unsigned)((ka[i] >> shift) & 0xFF)], 1u);
-    __syncthreads();
-    if (warp == 0) {  // exclusive scan of the 256 digit counts (8 per lane)
-      unsigned int c[8], tot = 0;
+    // ka/va were written by this CTA in the previous pass (ordered by the barrier below):
+    // plain loads, not the read-only path; the scatter walk re-reads the segment (L1 hits)
+    // instead of holding it in registers across the scan, G keys per lane at a time
 #pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        c[q] = run[lane * 8 + q];
-        tot += c[q];
+    for (int q = 0; q < 8; ++q) row[lane * 8 + q] = 0u;
+    __syncwarp();
+#pragma unroll
+    for (int g0 = 0; g0 < ITEMS; g0 += ITEMS) {  // all the segment's loads together: one latency
+      K key[ITEMS];
+#pragma unroll
+      for (int j = 0; j < ITEMS; ++j) key[j] = seg + (g0 + j) * 32 < n ? ka[seg + (g0 + j) * 32] : K(0);
+#pragma unroll
+      for (int j = 0; j < ITEMS; ++j) {
+        const bool valid = seg + (g0 + j) * 32 < n;
+        const unsigned d = valid ? (unsigned)((key[j] >> shift) & 0xFF) : 256u;
+        const unsigned peers = __match_any_sync(0xFFFFFFFFu, d);
+        if (valid && (peers & lt_mask) == 0u) atomicAdd(&row[d], (unsigned)__popc(peers));
+      }
+    }
+    __syncthreads();
+    {  // exclusive scan over (digit, warp), digit-major: thread t owns digit t / TPD and 8 warps
+      const int d = tid / TPD, w0 = (tid % TPD) * 8;
+      unsigned int c[8], tot = 0u;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        c[j] = cnt[(w0 + j) * kSortCntStride + d];
+        tot += c[j];
       }
       unsigned int inc = tot;
 #pragma unroll
@@ -169,47 +202,71 @@ __global__ void __launch_bounds__(1024) k_radix_sort_cta(K* __restrict__ ka, uin
         const unsigned int t = __shfl_up_sync(0xFFFFFFFFu, inc, o);
         if (lane >= o) inc += t;
       }
-      unsigned int acc = inc - tot;
+      if (lane == 31) wsum[warp] = inc;
+      __syncthreads();
+      if (warp == 0) {
+        const unsigned int ws = lane < NW ? wsum[lane] : 0u;
+        unsigned int wi = ws;
 #pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        run[lane * 8 + q] = acc;
-        acc += c[q];
+        for (int o = 1; o < 32; o <<= 1) {
+          const unsigned int t = __shfl_up_sync(0xFFFFFFFFu, wi, o);
+          if (lane >= o) wi += t;
+        }
+        if (lane < NW) wsum[lane] = wi - ws;
+      }
+      __syncthreads();
+      unsigned int acc = wsum[warp] + inc - tot;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        cnt[(w0 + j) * kSortCntStride + d] = acc;
+        acc += c[j];
       }
     }
     __syncthreads();
-    for (int base = 0; base < n; base += 1024) {
-      const int i = base + tid;
-      const bool valid = i < n;
-      const K key = valid ? ka[i] : K(0);
-      const uint32_t val = valid ? va[i] : 0u;
-      const unsigned digit = valid ? (unsigned)((key >> shift) & 0xFF) : 256u;
-      const unsigned peers = __match_any_sync(0xFFFFFFFFu, digit);
-      const unsigned rank = __popc(peers & lt_mask);
-      if (valid && rank == 0) wcnt[warp][digit] = __popc(peers);
-      __syncthreads();
-      if (tid < 256) {
-        unsigned int acc = run[tid];
-        for (int w = 0; w < 32; ++w) {
-          const unsigned int t = wcnt[w][tid];
-          wcnt[w][tid] = acc;
-          acc += t;
+#pragma unroll
+    for (int g0 = 0; g0 < ITEMS; g0 += G) {  // loads first (kb may alias ka for the compiler)
+      K key[G];
+      uint32_t val[G];
+#pragma unroll
+      for (int j = 0; j < G; ++j) {
+        const bool valid = seg + (g0 + j) * 32 < n;
+        key[j] = valid ? ka[seg + (g0 + j) * 32] : K(0);
+        val[j] = valid ? va[seg + (g0 + j) * 32] : 0u;
+      }
+#pragma unroll
+      for (int j = 0; j < G; ++j) {
+        const bool valid = seg + (g0 + j) * 32 < n;
+        const unsigned d = valid ? (unsigned)((key[j] >> shift) & 0xFF) : 256u;
+        const unsigned peers = __match_any_sync(0xFFFFFFFFu, d);
+        const unsigned rank = (unsigned)__popc(peers & lt_mask);
+        unsigned base = 0u;
+        if (valid && rank == 0u) base = atomicAdd(&row[d], (unsigned)__popc(peers));
+        base = __shfl_sync(0xFFFFFFFFu, base, __ffs(peers) - 1);
+        if (valid) {
+          kb[base + rank] = key[j];
+          vb[base + rank] = val[j];
         }
-        run[tid] = acc;
       }
-      __syncthreads();
-      if (valid) {
-        const unsigned pos = wcnt[warp][digit] + rank;
-        kb[pos] = key;
-        vb[pos] = val;
-      }
-      __syncthreads();
-      if (tid < 256)
-        for (int w = 0; w < 32; ++w) wcnt[w][tid] = 0;
-      __syncthreads();
     }
+    __syncthreads();  // the scattered pass is visible to every warp before the next pass loads it
     K* tk = ka; ka = kb; kb = tk;
     uint32_t* tv = va; va = vb; vb = tv;
   }
+}
+
+template <typename K>
+inline void launch_sort_cta(K* k0, uint32_t* v0, K* k1, uint32_t* v1, int n, int key_bits, cudaStream_t stream) {
+  constexpr int T = kSortCtaThreads;
+  if (n <= T)
+    k_radix_sort_cta<K, 1><<<1, T, 0, stream>>>(k0, v0, k1, v1, n, key_bits);
+  else if (n <= 2 * T)
+    k_radix_sort_cta<K, 2><<<1, T, 0, stream>>>(k0, v0, k1, v1, n, key_bits);
+  else if (n <= 4 * T)
+    k_radix_sort_cta<K, 4><<<1, T, 0, stream>>>(k0, v0, k1, v1, n, key_bits);
+  else if (n <= 8 * T)
+    k_radix_sort_cta<K, 8><<<1, T, 0, stream>>>(k0, v0, k1, v1, n, key_bits);
+  else
+    k_radix_sort_cta<K, 16><<<1, T, 0, stream>>>(k0, v0, k1, v1, n, key_bits);
 }
 
 // kernels radix_sort_pairs launches for n keys of key_bits bits
@@ -228,7 +285,7 @@ inline cudaError_t radix_sort_pairs(K* k0, uint32_t* v0, K* k1, uint32_t* v1, in
   *result_in_1 = false;
   if (n <= 1) return cudaSuccess;
   if (n <= kSortCtaMax) {
-    k_radix_sort_cta<K><<<1, 1024, 0, stream>>>(k0, v0, k1, v1, (int)n, key_bits);
+    launch_sort_cta<K>(k0, v0, k1, v1, (int)n, key_bits, stream);
     *result_in_1 = ((key_bits / 8) & 1) != 0;
     return cudaGetLastError();
   }

@@ -553,12 +553,28 @@ int spasm_solve_al(const spasm_traj* t, int dtype, const spasm_al_config* cfg, c
   else
     st = launch_solve_al<double>(*t, prm, (const double*)values, P, rec, lift_status, (double*)best_values, res_dev,
                                  s);
+  Traj& tm = const_cast<spasm_traj&>(*t);  // the pinned staging is the handle's internal cache
+  tm.best_nv = -1;
+  const int64_t nv = (int64_t)t->B * cfg->waypoints * t->J;
+  if (st == SPASM_OK && best_values && tm.pinned_bytes < kAlBestOffset + (size_t)nv * 8) {
+    // grow the staging so the accepted trajectory rides the one D2H below (every solve syncs
+    // before it returns, so no copy still targets the old buffer)
+    void* grown = nullptr;
+    size_t got = 0;
+    if (pinned_get(&grown, kAlBestOffset + (size_t)nv * 8, &got) != cudaSuccess) {
+      st = SPASM_ERR_CUDA;
+    } else {
+      pinned_put(tm.pinned, tm.pinned_bytes);
+      tm.pinned = grown;
+      tm.pinned_bytes = got;
+    }
+  }
+  double* best64 = nullptr;
   if (st == SPASM_OK && best_values) {
     // the float64 re-check of the accepted trajectory, queued behind the solve (its result
     // joins the one D2H copy below); on failure best_values holds no trajectory and the
     // check is ignored
-    const int64_t nv = (int64_t)t->B * cfg->waypoints * t->J;
-    double* best64 = reinterpret_cast<double*>(reinterpret_cast<char*>(ws) + L.best64);
+    best64 = reinterpret_cast<double*>(reinterpret_cast<char*>(ws) + L.best64);
     if (dtype == SPASM_F32) {
       k_widen<<<ceil_div(nv, 256), 256, 0, s>>>((const float*)best_values, nv, best64);
       if (cudaGetLastError() != cudaSuccess) st = SPASM_ERR_CUDA;
@@ -578,6 +594,11 @@ int spasm_solve_al(const spasm_traj* t, int dtype, const spasm_al_config* cfg, c
   cudaEventRecord(e1, s);
   AlResultBlock* host = reinterpret_cast<AlResultBlock*>(t->pinned);
   cudaError_t e = cudaMemcpyAsync(host, res_dev, sizeof(AlResultBlock), cudaMemcpyDeviceToHost, s);
+  // the float64 accepted trajectory rides the same sync (spasm_al_best_host): no second
+  // round trip for the caller's host copy of the result
+  if (e == cudaSuccess && best64)
+    e = cudaMemcpyAsync(static_cast<char*>(t->pinned) + kAlBestOffset, best64, (size_t)nv * 8, cudaMemcpyDeviceToHost,
+                        s);
   if (e == cudaSuccess) e = cudaStreamSynchronize(s);
   float ms = 0.f;
   if (e == cudaSuccess) cudaEventElapsedTime(&ms, e0, e1);
@@ -599,7 +620,16 @@ int spasm_solve_al(const spasm_traj* t, int dtype, const spasm_al_config* cfg, c
   result->checked_violation = host->check_violation;
   result->checked_feasible = host->check_feasible;
   result->reserved = 0;
+  if (best64 && host->status == SPASM_OK) tm.best_nv = nv;
   return host->status;
+}
+
+int spasm_al_best_host(const spasm_traj* t, double* out, int64_t n) {
+  SPASM_REQUIRE(t != nullptr && out != nullptr, "null argument");
+  SPASM_REQUIRE(t->best_nv >= 0, "no accepted trajectory staged (spasm_solve_al without best_values or not SPASM_OK)");
+  SPASM_REQUIRE(n == t->best_nv, "value count mismatch");
+  std::memcpy(out, static_cast<const char*>(t->pinned) + kAlBestOffset, (size_t)n * 8);
+  return SPASM_OK;
 }
 
 }  // extern "C"

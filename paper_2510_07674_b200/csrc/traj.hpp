@@ -21,6 +21,8 @@ struct Traj {
   const Model* twin = nullptr;    // free-yaw placement model (owned by the caller)
   void* pinned = nullptr;         // small result staging
   size_t pinned_bytes = 0;
+  int64_t best_nv = -1;           // float64 values of the last accepted trajectory staged after
+                                  // the result block (kAlBestOffset), -1 none (spasm_al_best_host)
   std::mutex mu;                  // guards the lazy device upload
 
   template <typename R> const TrajScene<R>* dev() const;
@@ -31,6 +33,9 @@ template <> inline const TrajScene<float>* Traj::dev<float>() const { return df;
 template <> inline const TrajScene<double>* Traj::dev<double>() const { return dd; }
 template <> inline const TrajScene<float>& Traj::host<float>() const { return hf; }
 template <> inline const TrajScene<double>& Traj::host<double>() const { return hd; }
+
+// pinned staging layout of spasm_solve_al: the result block, then the accepted trajectory
+constexpr size_t kAlBestOffset = 256;
 
 // result block of one AL solve (device -> pinned host)
 struct AlResultBlock {
@@ -48,5 +53,6 @@ struct AlResultBlock {
   uint8_t check_feasible;
   uint8_t pad[7];
 };
+static_assert(sizeof(AlResultBlock) <= kAlBestOffset, "result block overlaps the staged trajectory");
 
 }  // namespace spasm

@@ -614,6 +614,30 @@ def _particle_trajectory(values_p, geo: _Geometry) -> Trajectory:
     return Trajectory(segments=np.array(values_p, dtype=float), attached=att)
 
 
+def _best_host(geo, best):
+    """The accepted trajectory (B,T,J) as float64 host values, from the pinned staging the
+    AL solve's one D2H copy filled (spasm_al_best_host)."""
+    out = np.empty(tuple(best.shape), dtype=np.float64)
+    nat.check(geo._lib.spasm_al_best_host(geo.handle, out.ctypes.data, out.size), "spasm_al_best_host")
+    return out
+
+
+_PINNED = {}
+
+
+def _pinned_like(t):
+    """A cached pinned host tensor of t's shape and dtype (reused across solves: the caller
+    has read the previous contents by the time the next solve enqueues a copy into it)."""
+    torch = _torch()
+    key = (tuple(t.shape), t.dtype)
+    h = _PINNED.get(key)
+    if h is None:
+        if len(_PINNED) >= 16:
+            _PINNED.clear()
+        h = _PINNED[key] = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+    return h
+
+
 def _solve_al_device(geo, values_dev, config: TrajOptConfig, place_mode, precision, *, n_active=None,
                      lift_status=None, want_report=True):
     """Launch the persistent AL solve; returns (status, result struct, best (B,T,J) tensor, report)."""
@@ -786,6 +810,11 @@ def solve_stage2(scene, result, config, seed, trajopt_overrides, t0, precision: 
         lift = _lift_async(lift_geo, pl, seed, LIFT_CANDIDATES, precision)
     state = _pcg_state(trajectory_stream(seed))
     values = _init_async(geo, lift.endpoints, lift.status[1:], tcfg, state, precision)
+    # the kept-row list reaches pinned host memory in stream order ahead of the AL solve, and
+    # the accepted trajectory rides the AL solve's one D2H copy (spasm_al_best_host): no
+    # further round trip after the sync
+    kept_host = _pinned_like(lift.kept)
+    kept_host.copy_(lift.kept, non_blocking=True)
     status, res, best, report = _solve_al_device(geo, values, tcfg, None, precision, n_active=lift.status[1:],
                                                  lift_status=lift.status, want_report=False)
     if pending is not None:
@@ -800,14 +829,14 @@ def solve_stage2(scene, result, config, seed, trajopt_overrides, t0, precision: 
     if status == nat.SPASM_LIFT_FAILURE:
         return SceneSolution(False, time_ms, result.report.restarts, result.report.steps, math.nan, stats=stats,
                              bookkeeping={"lift_failed": True}), result
-    kept = lift.kept[:int(res.n_particles)].cpu().numpy()
+    kept = kept_host[:int(res.n_particles)].numpy().copy()
     book = {"kept": kept, "accepted_outer": int(res.accepted_outer), "al_particle": int(res.particle_index),
             "objective": float(res.objective), "lift_failed": False}
     if status == nat.SPASM_AL_FAILURE:
         w = float(res.least_violation)
         return SceneSolution(False, time_ms, result.report.restarts, result.report.steps, w, max_violation=w,
                              stats=stats, bookkeeping=book), result
-    traj = _particle_trajectory(best.double().cpu().numpy(), geo)
+    traj = _particle_trajectory(_best_host(geo, best), geo)
     # the independent float64 validate of the accepted trajectory (bench.py:249) ran on the
     # device behind the AL solve (spasm_solve_al: checked_feasible / checked_violation)
     feasible, worst = bool(res.checked_feasible), float(res.checked_violation)
@@ -837,7 +866,7 @@ def solve_motion_scene(scene, seed, trajopt_overrides, precision: str = "fp32"):
     if status == nat.SPASM_AL_FAILURE:
         w = float(res.least_violation)
         return SceneSolution(False, time_ms, 0, 0, w, max_violation=w, stats=stats)
-    traj = _particle_trajectory(best.double().cpu().numpy(), geo)
+    traj = _particle_trajectory(_best_host(geo, best), geo)
     feasible, worst = bool(res.checked_feasible), float(res.checked_violation)  # device float64 validate
     return SceneSolution(bool(feasible), time_ms, 0, 0, worst, trajectory=traj,
                          path_length=trajectory_path_length(traj), max_violation=worst, stats=stats)

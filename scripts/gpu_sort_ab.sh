@@ -1,0 +1,7 @@
+timeout 300 python scripts/sort_timing.py > gpurun_out/sort_new.txt 2>&1
+(cd _ab_old && timeout 300 python ../scripts/sort_timing.py > ../gpurun_out/sort_old.txt 2>&1)
+timeout 900 python -m pytest tests -m gpu -q -x 2>&1 | tail -5 > gpurun_out/pytest_sort.txt
+for rep in 1 2; do for w in c2 c1; do
+ timeout 400 python bench.py --steps 20 --warmup 3 --workload $w --no-cpu --no-sub > gpurun_out/ab_new_${w}_${rep}_s.json 2>&1
+ (cd _ab_old && timeout 400 python bench.py --steps 20 --warmup 3 --workload $w --no-cpu --no-sub > ../gpurun_out/ab_old_${w}_${rep}_s.json 2>&1)
+done; done

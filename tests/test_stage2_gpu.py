@@ -228,3 +228,18 @@ def test_device_recheck_equals_validate(name, precision):
         ok, worst = tj.validate(sol.trajectory, sc.problem, sc.chain, grasp=sc.grasp, static_centers=sc.obstacle_centers,
                                 static_radii=sc.obstacle_radii, epsilon=_cfg(sc).validation_epsilon, precision="fp64")
         assert sol.success == ok and sol.max_violation == worst
+
+
+@pytest.mark.parametrize("precision", ["fp64", "fp32"])
+def test_al_best_host_equals_device_result(precision):
+    """The accepted trajectory staged in pinned memory by spasm_solve_al's one D2H copy
+    (spasm_al_best_host) equals the device result widened to float64, bit for bit; a handle
+    with nothing staged refuses."""
+    sc = load_scene("tower4")
+    geo = tj._geometry(sc.problem, sc.chain, sc.grasp, sc.obstacle_centers, sc.obstacle_radii)
+    with pytest.raises(Exception):
+        tj._best_host(geo, torch.empty((geo.n_segments, 1, 1)))
+    v, _ = tj._device(G["pipe_tower4_init"], precision)
+    status, res, best, _ = tj._solve_al_device(geo, v.clone(), _cfg(sc), None, precision, want_report=False)
+    assert status == 0
+    np.testing.assert_array_equal(tj._best_host(geo, best), best.double().cpu().numpy())
