@@ -374,8 +374,9 @@ int spasm_al_profile(int enable, double* out);
 int spasm_al_profile_warps(double* out);
 /* Diagnostic: counters of the fp32 lift kernel k_ik_group, summed over CTAs (CTAs, cycles
  * to the last restart's IK, cycles to the end, max / winner IK iterations, winner polish
- * iterations after IK, speculatively completed polishes, all restarts' IK iterations).
- * enable 1/0; out (8 doubles, optional) receives and resets them. */
+ * iterations after IK, speculatively completed polishes, all restarts' IK iterations), then
+ * maxima over CTAs (cycles to the last restart's IK, cycles to the end, winner polish
+ * iterations, IK iterations). enable 1/0; out (12 doubles, optional) receives and resets them. */
 int spasm_ik_profile(int enable, double* out);
 
 /* Self-test of the fp32 branch-free math on the device (n pseudo-random inputs from seed):

@@ -44,16 +44,16 @@ extern "C" int spasm_al_profile_warps(double* out) {
   return SPASM_OK;
 }
 
-// Diagnostic: k_ik_group counters (stage2_kernels.cuh g_ik_prof). enable 1/0; out (8
+// Diagnostic: k_ik_group counters (stage2_kernels.cuh g_ik_prof). enable 1/0; out (12
 // doubles, optional) receives and resets them.
 extern "C" int spasm_ik_profile(int enable, double* out) {
   using namespace spasm;
   SPASM_CUDA_TRY(cudaMemcpyToSymbol(g_ik_prof_on, &enable, sizeof(int)));
   if (out) {
-    unsigned long long h[8];
+    unsigned long long h[12];
     SPASM_CUDA_TRY(cudaMemcpyFromSymbol(h, g_ik_prof, sizeof(h)));
-    for (int k = 0; k < 8; ++k) out[k] = (double)h[k];
-    static const unsigned long long z[8] = {0};
+    for (int k = 0; k < 12; ++k) out[k] = (double)h[k];
+    static const unsigned long long z[12] = {0};
     SPASM_CUDA_TRY(cudaMemcpyToSymbol(g_ik_prof, z, sizeof(z)));
   }
   return SPASM_OK;

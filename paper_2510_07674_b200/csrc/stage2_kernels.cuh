@@ -34,8 +34,10 @@ namespace spasm {
 // Diagnostic counters of k_ik_group (spasm_ik_profile), summed over CTAs while enabled:
 // [0] CTAs, [1] cycles to the last restart's IK, [2] cycles to the end, [3] max IK
 // iterations, [4] winner IK iterations, [5] winner polish iterations (post-IK part),
-// [6] winners polished speculatively to completion, [7] restarts' IK iterations (sum)
-static __device__ unsigned long long g_ik_prof[8];
+// [6] winners polished speculatively to completion, [7] restarts' IK iterations (sum); maxima
+// over CTAs: [8] cycles to the last restart's IK, [9] cycles to the end, [10] winner polish
+// iterations, [11] IK iterations
+static __device__ unsigned long long g_ik_prof[12];
 static __device__ int g_ik_prof_on;
 
 // orders this thread's earlier shared-memory writes (own CTA or a cluster peer's) before its
@@ -191,6 +193,7 @@ __global__ void __launch_bounds__(MAXT) k_ik_group(const TrajScene<R>* __restric
       *((volatile int*)best_p) = b;
       if (prof) {
         atomicAdd(&g_ik_prof[1], (unsigned long long)(clock64() - t_start));
+        atomicMax(&g_ik_prof[8], (unsigned long long)(clock64() - t_start));
         int mx = 0;
         unsigned long long sum = 0;
         for (int r = 0; r < restarts; ++r) {
@@ -198,6 +201,7 @@ __global__ void __launch_bounds__(MAXT) k_ik_group(const TrajScene<R>* __restric
           sum += its_p[r];
         }
         atomicAdd(&g_ik_prof[3], (unsigned long long)mx);
+        atomicMax(&g_ik_prof[11], (unsigned long long)mx);
         atomicAdd(&g_ik_prof[4], (unsigned long long)its_p[b]);
         atomicAdd(&g_ik_prof[7], sum);
       }
@@ -229,6 +233,7 @@ __global__ void __launch_bounds__(MAXT) k_ik_group(const TrajScene<R>* __restric
     }
     if (prof && lane0) {
       atomicAdd(&g_ik_prof[5], (unsigned long long)(pits + (spec_done ? spec_its : 0)));
+      atomicMax(&g_ik_prof[10], (unsigned long long)(pits + (spec_done ? spec_its : 0)));
       if (spec_done) atomicAdd(&g_ik_prof[6], 1ull);
     }
     pol = pol_spec;
@@ -237,6 +242,7 @@ __global__ void __launch_bounds__(MAXT) k_ik_group(const TrajScene<R>* __restric
   if (prof && lane0) {
     atomicAdd(&g_ik_prof[0], 1ull);
     atomicAdd(&g_ik_prof[2], (unsigned long long)(clock64() - t_start));
+    atomicMax(&g_ik_prof[9], (unsigned long long)(clock64() - t_start));
   }
   if (!tile_lane) return;
   if (tl.j < J) reinterpret_cast<R*>(out.sol)[(int64_t)grp * J + tl.j] = qj;

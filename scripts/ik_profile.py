@@ -15,7 +15,7 @@ scene = load_scene(scene_name)
 model = as_cost_model(scene.problem, precision="fp32")
 lib = nat.load()
 solve_scene(scene, seed=99, model=model)
-out = np.zeros(8)
+out = np.zeros(12)
 lib.spasm_ik_profile(1, None)
 lib.spasm_ik_profile(1, out.ctypes.data)  # reset
 for s in range(solves):
@@ -26,3 +26,5 @@ print(f"scene {scene_name}: {solves} solves, {out[0]:.0f} lift CTAs (groups); pe
 print(f"  cycles to the last restart's IK {out[1] / n:10.0f}   to the end {out[2] / n:10.0f}")
 print(f"  IK iterations: max over restarts {out[3] / n:.1f}, winner {out[4] / n:.1f}, mean {out[7] / n / 16:.1f}")
 print(f"  winner polish iterations (speculative + after IK) {out[5] / n:.1f}; polished speculatively to completion {out[6] / n * 100:.0f} %")
+print(f"  max over CTAs: cycles to the last restart's IK {out[8]:.0f}, to the end {out[9]:.0f}; "
+      f"IK iterations {out[11]:.0f}, winner polish iterations {out[10]:.0f}")
