@@ -10,6 +10,8 @@
 // (exclusive scan over digit x tile) -> k_radix_scatter (stable in-tile ranking with
 // __match_any_sync + per-warp digit counters, then scatter).
 #pragma once
+#include <cooperative_groups.h>
+
 #include "common.cuh"
 
 namespace spasm {
@@ -135,9 +137,10 @@ __global__ void __launch_bounds__(kSortThreads) k_radix_scatter(const K* __restr
   }
 }
 
-// Small batches (n <= kSortCtaMax): every pass in ONE CTA of 512 threads. Warp w owns the
-// contiguous segment [w * 32 * ITEMS, (w + 1) * 32 * ITEMS); lane l holds its positions seg + i * 32 + l (i < ITEMS: coalesced loads, batch i = 32
-// consecutive keys). Per 8-bit digit pass:
+// Small batches (n <= kSortCtaMax = 1024): every pass in ONE CTA of 512 threads. Warp w
+// owns the contiguous segment [w * 32 * ITEMS, (w + 1) * 32 * ITEMS); lane l holds its
+// positions seg + i * 32 + l (i < ITEMS: coalesced loads, batch i = 32 consecutive keys).
+// Per 8-bit digit pass:
 //   1. per-warp digit counts cnt[w][d] (__match_any_sync peers; the batch's leader adds),
 //   2. one exclusive scan over the counters in digit-major order (d, w): warp w's keys of
 //      digit d land after every earlier warp's keys of digit d and every smaller digit,
@@ -145,15 +148,12 @@ __global__ void __launch_bounds__(kSortThreads) k_radix_scatter(const K* __restr
 //      base by a shared atomicAdd on cnt[w][d] (one warp's atomics on an address are
 //      performed in issue order, so batch i precedes batch i+1) and broadcasts it; key i of
 //      the group goes to base + its rank among the group,
-// so every pass is stable and ties keep their index order (numpy's kind="stable"). Three CTA
-// barriers per pass, against four per 1024-key chunk and a serial 32-warp prefix before
-// (the satisfying-particle ordering of particle_opt.py:363 runs on m <= 8k keys every restart).
+// so every pass is stable and ties keep their index order (numpy's kind="stable"), with
+// three CTA barriers per pass. One CTA's MATCH / atomic issue bounds it (2k / 4k / 8k keys:
+// 24 / 34 / 50 us), so above 1k keys the cluster form below spreads the passes over SMs.
 constexpr int kSortCtaThreads = 512;
 constexpr int kSortCtaWarps = kSortCtaThreads / 32;
-// Above 8k keys the multi-CTA passes win (spasm_sort_pairs, scripts/sort_timing.py on B200:
-// 16k keys 87 us in one CTA against 67 us over 8 CTAs; the one-CTA form at 2k / 4k / 8k keys
-// 24 / 34 / 50 us against 26 / 38 / 62 us for the previous chunked single-CTA sort)
-constexpr int kSortCtaMax = kSortCtaThreads * 16;  // 8192
+constexpr int kSortCtaMax = 2 * kSortCtaThreads;  // 1024 (above: k_radix_sort_cluster)
 constexpr int kSortCntStride = 257;  // counter row stride: fewer bank conflicts in the digit-major scan
 
 template <typename K, int ITEMS>
@@ -259,20 +259,146 @@ inline void launch_sort_cta(K* k0, uint32_t* v0, K* k1, uint32_t* v1, int n, int
   constexpr int T = kSortCtaThreads;
   if (n <= T)
     k_radix_sort_cta<K, 1><<<1, T, 0, stream>>>(k0, v0, k1, v1, n, key_bits);
-  else if (n <= 2 * T)
-    k_radix_sort_cta<K, 2><<<1, T, 0, stream>>>(k0, v0, k1, v1, n, key_bits);
-  else if (n <= 4 * T)
-    k_radix_sort_cta<K, 4><<<1, T, 0, stream>>>(k0, v0, k1, v1, n, key_bits);
-  else if (n <= 8 * T)
-    k_radix_sort_cta<K, 8><<<1, T, 0, stream>>>(k0, v0, k1, v1, n, key_bits);
   else
-    k_radix_sort_cta<K, 16><<<1, T, 0, stream>>>(k0, v0, k1, v1, n, key_bits);
+    k_radix_sort_cta<K, 2><<<1, T, 0, stream>>>(k0, v0, k1, v1, n, key_bits);
+}
+
+// Mid-size batches (1024 < n <= kSortClusterMax): every pass in ONE launch of a thread-block
+// cluster of C CTAs of 256 threads, CTA c owning the keys [c T, (c + 1) T), T = 256 ITEMS
+// (ITEMS = 4 / 8 / 16 for n <= 8k / 16k / 64k; C <= 8, up to 16 through the non-portable
+// cluster size). Per pass each CTA forms per-warp digit counts over warp-contiguous
+// segments (as k_radix_sort_cta), its 256 threads (one per digit) sum them into the CTA's
+// histogram and publish it; after a cluster barrier every CTA reads the C histograms through
+// distributed shared memory, so digit d of CTA c starts at (keys of smaller digits anywhere)
+// + (keys of digit d in CTAs < c), and each warp scatters with atomic bases. A fence and a
+// second cluster barrier make the pass's global writes visible to the next pass's loads in
+// the other CTAs (and keep every CTA's histogram alive while its peers read it). One launch
+// replaces 12 (3 per pass) for the 16k-particle select of C2 / C4 and the 64k one of C3
+// (particle_opt.py:195-200): 16k keys 35 us against 71 us (scripts/sort_timing.py, B200).
+constexpr int kSortClThreads = 256;
+constexpr int kSortClusterMax = 16 * kSortClThreads * 16;  // 65536
+
+template <typename K, int ITEMS>
+__global__ void __launch_bounds__(kSortClThreads) k_radix_sort_cluster(K* ka, uint32_t* va, K* kb, uint32_t* vb,
+                                                                       int n, int key_bits) {
+  namespace cg = cooperative_groups;
+  cg::cluster_group cl = cg::this_cluster();
+  constexpr int NW = kSortClThreads / 32;
+  __shared__ unsigned int cnt[NW * kSortCntStride];
+  __shared__ unsigned int hist[256];
+  __shared__ unsigned int wsum[NW];
+  const int C = (int)cl.num_blocks(), c = (int)cl.block_rank();
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const unsigned lt_mask = (1u << lane) - 1u;
+  const int seg = c * kSortClThreads * ITEMS + warp * 32 * ITEMS + lane;
+  unsigned int* const row = cnt + warp * kSortCntStride;
+  for (int shift = 0; shift < key_bits; shift += 8) {
+    K key[ITEMS];
+    uint32_t val[ITEMS];
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) {  // written by the cluster in the previous pass: plain loads
+      const int pos = seg + i * 32;
+      key[i] = pos < n ? ka[pos] : K(0);
+      val[i] = pos < n ? va[pos] : 0u;
+    }
+#pragma unroll
+    for (int q = 0; q < 8; ++q) row[lane * 8 + q] = 0u;
+    __syncwarp();
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) {
+      const bool valid = seg + i * 32 < n;
+      const unsigned d = valid ? (unsigned)((key[i] >> shift) & 0xFF) : 256u;
+      const unsigned peers = __match_any_sync(0xFFFFFFFFu, d);
+      if (valid && (peers & lt_mask) == 0u) atomicAdd(&row[d], (unsigned)__popc(peers));
+    }
+    __syncthreads();
+    // thread d: the CTA's count of digit d, and each warp's exclusive prefix within the CTA
+    unsigned int wpre[NW], h = 0u;
+#pragma unroll
+    for (int w = 0; w < NW; ++w) {
+      wpre[w] = h;
+      h += cnt[w * kSortCntStride + tid];
+    }
+    hist[tid] = h;
+    cl.sync();  // every CTA's histogram of this pass is published
+    unsigned int tot = 0u, pre = 0u;
+    for (int r = 0; r < C; ++r) {
+      const unsigned int v = cl.map_shared_rank(hist, r)[tid];
+      tot += v;
+      pre += r < c ? v : 0u;
+    }
+    // exclusive scan of the cluster-wide digit totals over the 256 digits
+    unsigned int inc = tot;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned int t = __shfl_up_sync(0xFFFFFFFFu, inc, o);
+      if (lane >= o) inc += t;
+    }
+    if (lane == 31) wsum[warp] = inc;
+    __syncthreads();
+    unsigned int wbase = 0u;
+#pragma unroll
+    for (int w = 0; w < NW; ++w) wbase += w < warp ? wsum[w] : 0u;
+    const unsigned int base = wbase + inc - tot + pre;
+#pragma unroll
+    for (int w = 0; w < NW; ++w) cnt[w * kSortCntStride + tid] = base + wpre[w];
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) {
+      const bool valid = seg + i * 32 < n;
+      const unsigned d = valid ? (unsigned)((key[i] >> shift) & 0xFF) : 256u;
+      const unsigned peers = __match_any_sync(0xFFFFFFFFu, d);
+      const unsigned rank = (unsigned)__popc(peers & lt_mask);
+      unsigned b = 0u;
+      if (valid && rank == 0u) b = atomicAdd(&row[d], (unsigned)__popc(peers));
+      b = __shfl_sync(0xFFFFFFFFu, b, __ffs(peers) - 1);
+      if (valid) {
+        kb[b + rank] = key[i];
+        vb[b + rank] = val[i];
+      }
+    }
+    __threadfence();  // this pass's scatter is visible cluster-wide before the next pass loads
+    cl.sync();
+    K* tk = ka; ka = kb; kb = tk;
+    uint32_t* tv = va; va = vb; vb = tv;
+  }
+}
+
+template <typename K, int ITEMS>
+inline cudaError_t launch_sort_cluster_t(K* k0, uint32_t* v0, K* k1, uint32_t* v1, int n, int key_bits,
+                                         cudaStream_t stream) {
+  const unsigned C = (unsigned)((n + kSortClThreads * ITEMS - 1) / (kSortClThreads * ITEMS));
+  if (C > 8) {  // 9-16 CTAs: B200 schedules clusters of up to 16 once the kernel opts in
+    static const cudaError_t opt =
+        cudaFuncSetAttribute(k_radix_sort_cluster<K, ITEMS>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    if (opt != cudaSuccess) return opt;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(C);
+  cfg.blockDim = dim3(kSortClThreads);
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = C;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, k_radix_sort_cluster<K, ITEMS>, k0, v0, k1, v1, n, key_bits);
+}
+
+template <typename K>
+inline cudaError_t launch_sort_cluster(K* k0, uint32_t* v0, K* k1, uint32_t* v1, int n, int key_bits,
+                                       cudaStream_t stream) {
+  if (n <= 8 * kSortClThreads * 4) return launch_sort_cluster_t<K, 4>(k0, v0, k1, v1, n, key_bits, stream);
+  if (n <= 8 * kSortClThreads * 8) return launch_sort_cluster_t<K, 8>(k0, v0, k1, v1, n, key_bits, stream);
+  return launch_sort_cluster_t<K, 16>(k0, v0, k1, v1, n, key_bits, stream);
 }
 
 // kernels radix_sort_pairs launches for n keys of key_bits bits
 inline int radix_sort_launches(int64_t n, int key_bits) {
   if (n <= 1) return 0;
-  return n <= kSortCtaMax ? 1 : 3 * (key_bits / 8);
+  return n <= kSortClusterMax ? 1 : 3 * (key_bits / 8);
 }
 
 // Host driver. Sorts (k0, v0) by key bits [0, key_bits) into (k1, v1) ping-pong
@@ -288,6 +414,10 @@ inline cudaError_t radix_sort_pairs(K* k0, uint32_t* v0, K* k1, uint32_t* v1, in
     launch_sort_cta<K>(k0, v0, k1, v1, (int)n, key_bits, stream);
     *result_in_1 = ((key_bits / 8) & 1) != 0;
     return cudaGetLastError();
+  }
+  if (n <= kSortClusterMax) {
+    *result_in_1 = ((key_bits / 8) & 1) != 0;
+    return launch_sort_cluster<K>(k0, v0, k1, v1, (int)n, key_bits, stream);
   }
   const int nblocks = ceil_div(n, kSortTile);
   unsigned int* totals = hist + (int64_t)256 * nblocks;

@@ -96,9 +96,10 @@ def test_select_topk_matches_reference_stable_order():
     np.testing.assert_array_equal(po.select_topk(b, 2), [2, 0])
 
 
-# every single-CTA variant's boundary (512 x ITEMS keys, ITEMS 1..16) and the multi-CTA path
-@pytest.mark.parametrize("n", [1, 2, 31, 511, 512, 513, 1025, 2047, 2048, 2049, 4097, 8193, 16383, 16384, 16385,
-                               100000])
+# the single-CTA variants' boundaries (512 x ITEMS keys), the cluster form's CTA-count and
+# ITEMS boundaries (256 x ITEMS keys per CTA, up to 16 CTAs) and the multi-CTA path
+@pytest.mark.parametrize("n", [1, 2, 31, 511, 512, 513, 1024, 1025, 2047, 2048, 2049, 4097, 8192, 8193, 16383, 16384,
+                               16385, 32769, 61440, 65536, 65537, 100000])
 def test_device_sort_large_with_ties(n):
     rng = np.random.default_rng(n)
     for dt in (torch.float32, torch.float64):
