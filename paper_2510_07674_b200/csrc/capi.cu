@@ -80,6 +80,8 @@ const char* last_error() { return g_last_error.c_str(); }
 
 static int g_stage1_tile = -1;  // spasm_set_option("stage1_tile", ...)
 int stage1_tile_mode() { return g_stage1_tile; }
+static int g_tower_lanes = 0;  // spasm_set_option("tower_lanes", ...): 0 auto, 1/2/4/8 lanes per particle
+int tower_lanes_option() { return g_tower_lanes; }
 static int g_graphs = 1;       // spasm_set_option("graphs", ...): CUDA-graph the stage-1 restart
 static thread_local const RestartParams* g_restart_override = nullptr;
 const RestartParams* restart_override() { return g_restart_override; }
@@ -420,6 +422,7 @@ static int solve_launch(Model& m, const spasm_solve_config& cfg, const double* w
     key.sampler = cfg.sampler;
     key.n_warm = n_warm;
     key.tile = stage1_tile_mode();
+    key.tower_lanes = tower_lanes_option();
     const bool cached = m.gexec && std::memcmp(&key, &m.gkey, sizeof(key)) == 0;
     // capture only from the second solve with the same shapes: a model solved once (e.g. a
     // replanning tick's fresh model) never pays for a capture it would not reuse
@@ -765,6 +768,12 @@ int spasm_set_option(const char* key, int value) {
   if (std::strcmp(key, "graphs") == 0) {
     SPASM_REQUIRE(value == 0 || value == 1, "graphs must be 0 or 1");
     g_graphs = value;
+    return SPASM_OK;
+  }
+  if (std::strcmp(key, "tower_lanes") == 0) {
+    SPASM_REQUIRE(value == 0 || value == 1 || value == 2 || value == 4 || value == 8,
+                  "tower_lanes must be 0 (auto), 1, 2, 4 or 8");
+    g_tower_lanes = value;
     return SPASM_OK;
   }
   if (std::strcmp(key, "stage1_tile") == 0) {

@@ -25,6 +25,7 @@
 namespace spasm {
 
 int stage1_tile_mode();  // spasm_set_option("stage1_tile")
+int tower_lanes_option();  // spasm_set_option("tower_lanes")
 void seedseq_pcg64(uint64_t seed, const uint64_t* spawn_key, int n_spawn, uint64_t out[4]);
 
 // ---- launchers (explicitly instantiated in stage1_f32.cu / stage1_f64.cu) ----------

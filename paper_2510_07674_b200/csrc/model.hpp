@@ -63,6 +63,7 @@ struct Model {
     int p_return, max_restarts, sampler;
     int64_t n_warm;
     int tile;
+    int tower_lanes;
   } gkey{}, gkey_seen{};
   // the solve launched by spasm_solve_launch, until spasm_solve_collect (capi.cu)
   SolvePending pend;

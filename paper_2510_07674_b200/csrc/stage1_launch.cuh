@@ -16,6 +16,7 @@ const RestartParams* restart_override();
 // Stage-1 tile-kernel switch (spasm_set_option("stage1_tile", v)): -1 auto, 0 generic
 // kernel only, 1..4 force a tile variant (stage1tile_f32.cu).
 int stage1_tile_mode();
+int tower_lanes_option();
 // fp32 tetris tile schedule (stage1tile_f32.cu); returns -1 when not applicable.
 int launch_schedule_tile(const Model& m, const float* src, const uint32_t* rows, int64_t M, int k_lin, int k_quad,
                          double eta, double alpha, float* out_values, float* out_cost, uint8_t* flagged,

@@ -228,6 +228,7 @@ template <int LA>
 __device__ __forceinline__ float lane_sum(float v) {
   if constexpr (LA >= 2) v += __shfl_xor_sync(0xffffffffu, v, 1);
   if constexpr (LA >= 4) v += __shfl_xor_sync(0xffffffffu, v, 2);
+  if constexpr (LA >= 8) v += __shfl_xor_sync(0xffffffffu, v, 4);
   return v;
 }
 
