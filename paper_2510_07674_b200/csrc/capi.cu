@@ -82,6 +82,8 @@ static int g_stage1_tile = -1;  // spasm_set_option("stage1_tile", ...)
 int stage1_tile_mode() { return g_stage1_tile; }
 static int g_tower_lanes = 0;  // spasm_set_option("tower_lanes", ...): 0 auto, 1/2/4/8 lanes per particle
 int tower_lanes_option() { return g_tower_lanes; }
+static int g_ik_cluster = 0;  // spasm_set_option("ik_cluster", ...): 0 auto, 1/2/4/8 CTAs per lift group
+int ik_cluster_option() { return g_ik_cluster; }
 static int g_graphs = 1;       // spasm_set_option("graphs", ...): CUDA-graph the stage-1 restart
 static thread_local const RestartParams* g_restart_override = nullptr;
 const RestartParams* restart_override() { return g_restart_override; }
@@ -768,6 +770,12 @@ int spasm_set_option(const char* key, int value) {
   if (std::strcmp(key, "graphs") == 0) {
     SPASM_REQUIRE(value == 0 || value == 1, "graphs must be 0 or 1");
     g_graphs = value;
+    return SPASM_OK;
+  }
+  if (std::strcmp(key, "ik_cluster") == 0) {
+    SPASM_REQUIRE(value == 0 || value == 1 || value == 2 || value == 4 || value == 8,
+                  "ik_cluster must be 0 (auto), 1, 2, 4 or 8");
+    g_ik_cluster = value;
     return SPASM_OK;
   }
   if (std::strcmp(key, "tower_lanes") == 0) {

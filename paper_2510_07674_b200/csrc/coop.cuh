@@ -371,10 +371,10 @@ struct PolishRun {
   }
 };
 
-// The whole polish of one configuration. Optional speculative mode (k_ik_group): `best`
-// points at a shared slot that becomes the winning tile's index once every restart has
-// finished IK; a tile whose index `me` lost stops polishing (its result is discarded, so
-// the winner's result is unchanged). The slots are polled one step ahead of their test, so a
+// The whole polish of one configuration. Optional speculative mode (k_ik_group, a whole
+// warp per tile): `best` points at a shared slot that becomes the winning tile's index once
+// every restart has finished IK; a tile whose index `me` lost stops polishing (its result is
+// discarded, so the winner's result is unchanged). The slots are polled one step ahead of their test, so a
 // losing tile may run one step more than necessary.
 template <typename R>
 __device__ bool tile_polish(const Tile& tl, const ChainDesc<R>& ch, R& q_io, const R tp[3], R ty,
@@ -389,15 +389,17 @@ __device__ bool tile_polish(const Tile& tl, const ChainDesc<R>& ch, R& q_io, con
   unsigned long long c_seen = mine;
   for (;;) {
     if (best) {  // abort once another tile is the winner or the current best candidate
+      // polled by the warp's lane 0 only, the lane that published this restart's key into
+      // *cur (another lane's load is not ordered after that atomic); the vote spreads it
+      const bool poller = (threadIdx.x & 31) == 0;
       int stop = 0;
-      if (tl.j == 0) stop = (b_seen >= 0) ? (b_seen != me) : (cur != nullptr && c_seen != mine);
-      // any replica's lane 0 seeing the stop condition stops the whole tile / warp together
+      if (poller) stop = (b_seen >= 0) ? (b_seen != me) : (cur != nullptr && c_seen != mine);
       if (tl.any(stop != 0)) {
         q_io = qj;
         return false;
       }
       // poll now, test after this step: the (possibly cluster-remote) loads overlap the step
-      if (tl.j == 0) {
+      if (poller) {
         b_seen = *best;
         if (cur != nullptr) c_seen = *cur;
       }

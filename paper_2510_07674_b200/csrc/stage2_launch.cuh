@@ -5,6 +5,10 @@
 #include "traj.hpp"
 
 namespace spasm {
+int ik_cluster_option();  // spasm_set_option("ik_cluster") (capi.cu)
+}
+
+namespace spasm {
 
 // Calls f(std::integral_constant<int, KIND>{}, twin scene) for the handle's twin family.
 template <typename R, class F>
@@ -176,6 +180,7 @@ int launch_ik(const Traj& tr, int n_targets, int n_draws, uint64_t seed, uint64_
       cs = c;
     }
   }
+  if (ik_cluster_option() > 0) cs = ik_cluster_option() < restarts ? ik_cluster_option() : restarts;
   const int rpc = (restarts + cs - 1) / cs;
   const int bs = rpc * 32;  // one warp per restart tile
   cudaLaunchConfig_t cfg = {};

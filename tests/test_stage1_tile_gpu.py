@@ -58,6 +58,7 @@ def _rows(o, n, seed):
 def test_set_option_rejects_bad_values():
     lib = nat.load()
     assert lib.spasm_set_option(b"stage1_tile", 9) == nat.SPASM_ERR_USAGE
+    assert lib.spasm_set_option(b"tower_lanes", 3) == nat.SPASM_ERR_USAGE
     assert lib.spasm_set_option(b"no_such_option", 0) == nat.SPASM_ERR_USAGE
 
 
@@ -165,3 +166,31 @@ def test_tile_sample_eval_matches_generic_and_oracle(name):
     c_tile = _key_to_cost(out[-1][1])
     np.testing.assert_allclose(c_tile, _key_to_cost(out[0][1]), rtol=1e-4, atol=1e-6)
     np.testing.assert_allclose(c_tile, o.evaluate(out[-1][0], "linear"), rtol=1e-4, atol=1e-6)
+
+
+@pytest.mark.parametrize("name", ["tower4", "tower3c", "tower6r"])
+def test_tower_lane_counts_agree(name):
+    """The tower tile kernel with 1 / 2 / 4 / 8 lanes per particle (spasm_set_option
+    "tower_lanes"; auto picks by obstacle count) differs only in the order of the
+    cube-obstacle partial sums: one descent step agrees to fp32 rounding, and the full
+    schedule's flags are identical."""
+    lib = nat.load()
+    scene = load_scene(name)
+    m = as_cost_model(scene.problem, precision="fp32")
+    o = orc.oracle_model(scene.problem)
+    x = _rows(o, 2048, 11)
+    over = scene.solver_overrides
+    try:
+        runs = {}
+        for la in (1, 2, 4, 8):
+            nat.check(lib.spasm_set_option(b"tower_lanes", la), "set_option")
+            one = _schedule(m, x, 1, 0, over["eta_init"], over["alpha"])
+            full = _schedule(m, x, over["k_lin"], over["k_quad"], over["eta_init"], over["alpha"])
+            runs[la] = (one, full)
+        v4, c4 = runs[4][0][0], runs[4][0][1]
+        for la, ((v, c, _), (_, _, fl)) in runs.items():
+            np.testing.assert_allclose(v, v4, rtol=1e-5, atol=1e-6)
+            np.testing.assert_allclose(c, c4, rtol=1e-4, atol=1e-6)
+            np.testing.assert_array_equal(fl, runs[4][1][2])
+    finally:
+        nat.check(lib.spasm_set_option(b"tower_lanes", 0), "set_option")

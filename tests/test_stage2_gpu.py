@@ -243,3 +243,33 @@ def test_al_best_host_equals_device_result(precision):
     status, res, best, _ = tj._solve_al_device(geo, v.clone(), _cfg(sc), None, precision, want_report=False)
     assert status == 0
     np.testing.assert_array_equal(tj._best_host(geo, best), best.double().cpu().numpy())
+
+
+@pytest.mark.parametrize("name", ["tower3c", "tetris5", "single1"])
+def test_lift_invariant_to_cluster_size(name):
+    """The lift kernel deals each group's restarts over a thread-block cluster (selection
+    slots in rank 0's shared memory); the winners, their polished solutions and the kept set
+    must not depend on the cluster size (spasm_set_option "ik_cluster")."""
+    from paper_2510_07674_b200 import _native as nat
+    from paper_2510_07674_b200 import particle_opt as po
+    from paper_2510_07674_b200.problems import as_cost_model
+
+    lib = nat.load()
+    sc = load_scene(name)
+    model = as_cost_model(sc.problem, precision="fp32")
+    res = po.solve(model, po.OptimizerConfig(**{**sc.solver_overrides, "seed": 3}))
+    assert res.success
+    outs = {}
+    try:
+        for cs in (1, 2, 4, 8):
+            nat.check(lib.spasm_set_option(b"ik_cluster", cs), "set_option")
+            for seed in range(4):
+                r = tj.lift_placements(sc.problem, res.particles, sc.chain, sc.grasp, seed=seed,
+                                       static_centers=sc.obstacle_centers, static_radii=sc.obstacle_radii,
+                                       precision="fp32")
+                outs[cs, seed] = (r.kept, r.endpoints)
+    finally:
+        nat.check(lib.spasm_set_option(b"ik_cluster", 0), "set_option")
+    for (cs, seed), (kept, ends) in outs.items():
+        np.testing.assert_array_equal(kept, outs[1, seed][0])
+        np.testing.assert_array_equal(ends, outs[1, seed][1])
