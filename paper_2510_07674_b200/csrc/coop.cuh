@@ -379,14 +379,14 @@ struct PolishRun {
 template <typename R>
 __device__ bool tile_polish(const Tile& tl, const ChainDesc<R>& ch, R& q_io, const R tp[3], R ty,
                             const volatile int* best = nullptr, int me = 0,
-                            const volatile unsigned long long* cur = nullptr, unsigned long long mine = 0,
+                            const volatile unsigned* cur = nullptr, unsigned mine = 0,
                             bool* completed = nullptr, int* iters = nullptr) {
   if (completed) *completed = false;
   R qj = q_io;  // iterate in a register (q_io may live in memory when this is not inlined)
   PolishRun<R> run;
   run.begin(tl, ch, qj);
   int b_seen = -1;                 // the slots as of the last poll (this tile just led)
-  unsigned long long c_seen = mine;
+  unsigned c_seen = mine;
   for (;;) {
     if (best) {  // abort once another tile is the winner or the current best candidate
       // polled by the warp's lane 0 only, the lane that published this restart's key into

@@ -110,14 +110,14 @@ __global__ void __launch_bounds__(MAXT) k_ik_group(const TrajScene<R>* __restric
   __shared__ R s_key[32], s_score[32];
   __shared__ int s_ok[32];
   __shared__ int s_best, s_done;
-  __shared__ unsigned long long s_cur;  // best (approximate key, restart) among finished restarts
+  __shared__ unsigned int s_cur;  // best fp32-image key among finished restarts (speculation)
   __shared__ int s_its[32];
   const bool prof = g_ik_prof_on != 0;
   const long long t_start = prof ? clock64() : 0;
   if (threadIdx.x == 0 && crank == 0) {
     s_best = -1;
     s_done = 0;
-    s_cur = ~0ull;
+    s_cur = ~0u;
   }
   const TrajScene<R>& sc = *g_scene;
   {
@@ -133,7 +133,7 @@ __global__ void __launch_bounds__(MAXT) k_ik_group(const TrajScene<R>* __restric
   volatile int* const its_p = cl.map_shared_rank(s_its, 0);
   int* const best_p = cl.map_shared_rank(&s_best, 0);
   int* const done_p = cl.map_shared_rank(&s_done, 0);
-  unsigned long long* const cur_p = cl.map_shared_rank(&s_cur, 0);
+  unsigned int* const cur_p = cl.map_shared_rank(&s_cur, 0);
   const ChainDesc<R>& ch = ch_s;
   const int a = grp / n_targets, t = grp - a * n_targets;
   const int J = ch.J;
@@ -172,8 +172,13 @@ __global__ void __launch_bounds__(MAXT) k_ik_group(const TrajScene<R>* __restric
     const bool ok = tile_ik<R>(tl, ch, qj, tp, ty, max_iters, R(damping), &score, &its);
     if (prof && lane0) its_p[tile] = its;
     const R key = (ok ? R(0) : R(1e6)) + score;
-    // speculation order: (fp32 image of the key, restart); the exact winner is s_best below
-    const unsigned long long mine = ((unsigned long long)order_key((float)key) << 32) | (unsigned)tile;
+    // speculation order: the fp32 image of the key; the exact winner is s_best below
+    // A 32-bit slot: a 64-bit atomicMin on a cluster peer's shared memory did not behave as
+    // one (about 1 in 12 winners then saw a larger key replace its own and dropped its
+    // speculative polish; scripts/ik_cluster_sweep.py), 32-bit shared atomics are native. A
+    // restart whose key ties the leader's does not lead (strict <); the exact first-minimum
+    // winner is still s_best, and a winner that did not polish speculatively polishes after.
+    const unsigned mine = order_key((float)key);
     int last = 0, lead = 0;
     if (lane0) {
       key_p[tile] = key;

@@ -168,14 +168,14 @@ int launch_ik(const Traj& tr, int n_targets, int n_draws, uint64_t seed, uint64_
   const int64_t groups = (int64_t)n_targets * n_draws;
   // cluster size: spread each group's restart warps over CS CTAs (k_ik_group) so that the
   // busiest SM carries the fewest restart warps, assuming the CTAs spread evenly over the
-  // SMs (CS in {1, 2, 4, 8}, the smallest on ties; 1 when the grid is too large to gain)
+  // SMs (CS in {1, 2, 4, 8}, the largest on ties: more SMs share the same worst load)
   int cs = 1;
   int64_t best_load = INT64_MAX;
   for (int c = 1; c <= 8; c *= 2) {
     const int rpc = (restarts + c - 1) / c;
     if (c > restarts || groups * c > (int64_t)1 << 30) break;
     const int64_t load = ((groups * c + kNumSMs - 1) / kNumSMs) * rpc;
-    if (load < best_load) {
+    if (load <= best_load) {
       best_load = load;
       cs = c;
     }
